@@ -1,0 +1,143 @@
+/* fhtb200.h -- C ABI of libfhtb200.so, the B200 (sm_100a, fp64) engine behind
+ * the fasthankel-compatible Python package paper_1501_01652_b200.
+ *
+ * The reference (fasthankel, pure Python/NumPy) has no FFI of its own: its
+ * "operator API" is the Python function surface (__init__.py:44-85).  Each
+ * entry point below replaces the N-length numerical core of one reference
+ * function; the cited file:line is the reference code it stands in for.
+ * All array arguments are DEVICE pointers (fp64, row-major, batch-leading);
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ * asynchronous on `stream` unless stated otherwise.  Return value: FHTB_OK
+ * or an FHTB_E* code; fhtb_last_error() gives a thread-local message.
+ */
+#ifndef FHTB200_H
+#define FHTB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FHTB_OK 0
+#define FHTB_EINVAL 1      /* bad argument            -> Python ValueError   */
+#define FHTB_ECUDA 2       /* CUDA launch/runtime     -> Python RuntimeError */
+#define FHTB_ENONFINITE 3  /* non-finite result       -> Python RuntimeError */
+#define FHTB_ECONVERGE 4   /* Newton did not converge -> Python RuntimeError */
+
+#define FHTB_DCT1 0
+#define FHTB_DST1 1
+
+/* apply flags */
+#define FHTB_FAR 1         /* asymptotic blocks (DCT-I/DST-I far field)     */
+#define FHTB_NEAR 2        /* pointwise border segments (near field)        */
+#define FHTB_OVERWRITE 4   /* direct: F = result instead of F += result     */
+
+int fhtb_abi_version(void);
+const char* fhtb_last_error(void);
+/* Prepare per-device tables (twiddles, Bessel order constants) on the
+ * current device.  Idempotent; synchronous. */
+int fhtb_init(void);
+/* Tunables: "far_chunk_bytes" (two-pass intermediate budget). */
+int fhtb_set_option(const char* key, int64_t value);
+
+/* ---------------------------------------------------------------- L1 --- */
+/* out[i] = J_nu(z[i]); replaces bessel.py:232-260 (bessel_j, array path). */
+int fhtb_bessel_j(int nu, const double* z, int64_t n, double* out, void* stream);
+/* out[o*n + i] = J_o(z[i]) for o <= nu_max (one Miller sweep). */
+int fhtb_bessel_j_multi(int nu_max, const double* z, int64_t n, double* out, void* stream);
+/* replaces bessel.py:72-91 (hankel_asy_eval) */
+int fhtb_hankel_asy_eval(int nu, int m_terms, const double* z, int64_t n, double* out, void* stream);
+/* replaces bessel.py:133-146 (taylor_eval) */
+int fhtb_taylor_eval(int nu, int n_terms, const double* z, int64_t n, double* out, void* stream);
+/* First `count` roots of J0 and b_n = j_{0,n} - (n-1/4)pi; replaces
+ * bessel.py:295-321.  Synchronous: *resid_max (host) = max |J0(root)|;
+ * returns FHTB_ECONVERGE when it exceeds 1e-13 (bessel.py:313-317). */
+int fhtb_roots_j0(int64_t count, double* roots, double* perturb, double* resid_max, void* stream);
+/* Batched complex FFT (interleaved re/im), n = 2^k <= 2048, X_k = sum x_n e^{sign 2 pi i nk/n}.
+ * Utility behind the FFT-core tests. */
+int fhtb_fft(int64_t n, int sign, const double* in, double* out, int64_t batch, void* stream);
+/* DCT-I / DST-I of `batch` rows of length `length`; replaces trig.py:80-92
+ * (apply) for real rows.  Workspace from fhtb_trig_workspace. */
+size_t fhtb_trig_workspace(int kind, int64_t length, int64_t batch);
+int fhtb_trig_apply(int kind, int64_t length, const double* v, int64_t batch, double* out,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------ L2 engine ----- */
+/* A grid = the partitioned Schlomilch matrix of one (L, gamma, eps, order
+ * universe) problem: schlomilch.py:139-170 (build_partition) plus the
+ * _AsyWork state of schlomilch.py:244-270, kept on the device. */
+typedef struct fhtb_grid fhtb_grid;
+
+typedef struct fhtb_grid_desc {
+  int64_t L;                 /* grid length N (or 4N+3 for the DHT)          */
+  double gamma;              /* frequency shift: omega_n = (n+gamma) pi      */
+  int32_t m_terms;           /* M: 2M asymptotic terms per block             */
+  int32_t n_blocks;          /* blocks[4*b..]: r0, r1, c0, c1 (1-based, half-open) */
+  const int64_t* blocks;     /* host */
+  int32_t n_segments;        /* segments[3*s..]: r0, r1, c_end               */
+  const int64_t* segments;   /* host */
+  int64_t row_first;         /* output j <-> grid row k = row_first + row_stride*j */
+  int64_t row_stride;
+  int64_t n_out;
+  int64_t n_data_cols;       /* columns n > n_data_cols hold zero coefficients */
+  int32_t n_orders;          /* order universe (schlomilch.py:422-431)       */
+  const int32_t* orders;     /* host */
+} fhtb_grid_desc;
+
+/* One (order_weights, coefficients) request (schlomilch.py:436-468) with the
+ * fused diagonal pre/post multipliers of fourier_bessel.py:215-242 and
+ * dht.py:151-174:  x_n = C[vec][n-1] * pre_a[n-1]^pre_a_pow * pre_b[n-1]^pre_b_pow
+ * for n >= col_lo;  F[vec][j] += (k/L)^post_r_pow * post_e[j]^post_e_pow * y_k. */
+typedef struct fhtb_request {
+  int32_t vec;
+  int32_t n_terms;           /* weighted orders */
+  const int32_t* orders;     /* host, each in the grid universe */
+  const double* weights;     /* host */
+  int64_t col_lo;
+  const double* pre_a;       /* device or NULL */
+  int32_t pre_a_pow;
+  const double* pre_b;
+  int32_t pre_b_pow;
+  int32_t post_r_pow;
+  const double* post_e;      /* device or NULL, indexed by output j */
+  int32_t post_e_pow;
+} fhtb_request;
+
+int fhtb_grid_create(const fhtb_grid_desc* desc, fhtb_grid** out);
+void fhtb_grid_destroy(fhtb_grid* g);
+size_t fhtb_apply_workspace(const fhtb_grid* g, int32_t n_req, int32_t n_vec, int32_t flags);
+/* F[vec][j] += Schlomilch application of each request (far and/or near
+ * field per flags).  F must be initialised by the caller (zeros for a plain
+ * evaluation).  Deterministic reduction order. */
+int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C,
+               int64_t ldc, int32_t n_vec, double* F, int64_t ldf, int32_t flags, void* ws,
+               size_t ws_bytes, void* stream);
+
+/* Direct sums with rank-1 arguments z = row_val[k] * col_val[n] over a full
+ * n_rows x n_cols rectangle: fourier_bessel.py:148-172 (low columns),
+ * dht.py:82-94 (direct rows), and the O(N^2) oracles schlomilch.py:223-229,
+ * fourier_bessel.py:292-309.  Requests use the same structure (orders must
+ * be in the given universe; col_lo, pre/post as above, post_r_pow uses
+ * k/r_scale). */
+typedef struct fhtb_direct_desc {
+  int64_t n_rows;
+  const double* row_val;     /* device */
+  int64_t n_cols;
+  const double* col_val;     /* device */
+  int64_t n_data_cols;
+  double r_scale;
+  int32_t n_orders;
+  const int32_t* orders;     /* host */
+} fhtb_direct_desc;
+
+size_t fhtb_direct_workspace(const fhtb_direct_desc* d, int32_t n_req, int32_t n_vec);
+int fhtb_direct_apply(const fhtb_direct_desc* d, const fhtb_request* reqs, int32_t n_req,
+                      const double* C, int64_t ldc, int32_t n_vec, double* F, int64_t ldf,
+                      int32_t flags, void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FHTB200_H */

@@ -1,0 +1,117 @@
+"""Device plumbing: torch tensors for memory/streams, workspace cache.
+
+PyTorch is used only to own device memory, pick the current stream and move
+host arrays; every numerical operation on N-length data runs in
+libfhtb200.so.
+"""
+
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+
+_ws_lock = threading.Lock()
+_ws = {}
+
+
+def device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1501_01652_b200 needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr():
+    return ctypes_void(torch.cuda.current_stream().cuda_stream)
+
+
+def ctypes_void(x):
+    return x if x else None
+
+
+def ptr(t):
+    return t.data_ptr() if t is not None else None
+
+
+_inited = set()
+
+
+def ensure_init():
+    dev = device()
+    if dev.index not in _inited:
+        _lib.load()
+        _lib.call("fhtb_init")
+        _inited.add(dev.index)
+    return dev
+
+
+def workspace(nbytes):
+    """A cached uint8 device buffer of at least nbytes (per device/stream)."""
+    dev = device()
+    key = (dev.index, torch.cuda.current_stream().cuda_stream)
+    with _ws_lock:
+        buf = _ws.get(key)
+        if buf is None or buf.numel() < nbytes:
+            if buf is not None:
+                del _ws[key]
+                buf = None
+            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
+            _ws[key] = buf
+    return buf
+
+
+def to_dev_f64(x, dev=None):
+    """Host array-like / tensor -> contiguous float64 CUDA tensor."""
+    dev = dev or device()
+    if isinstance(x, torch.Tensor):
+        return x.to(device=dev, dtype=torch.float64).contiguous()
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    return torch.from_numpy(a).to(dev, non_blocking=False)
+
+
+def as_real_batch(c):
+    """Split coefficients into a real (B, N) float64 device tensor.
+
+    Returns (tensor, meta) where meta records how to rebuild the caller's
+    shape/dtype: complex inputs become two real rows (real, imag) per vector
+    (the transforms are real-linear, test_schlomilch.py:256-264).
+    """
+    is_torch = isinstance(c, torch.Tensor)
+    if is_torch:
+        cplx = c.is_complex()
+        arr = c
+    else:
+        arr = np.asarray(c)
+        cplx = np.iscomplexobj(arr)
+        if not cplx and not np.issubdtype(arr.dtype, np.floating):
+            arr = arr.astype(np.float64)
+    one = arr.ndim == 1
+    if arr.ndim not in (1, 2):
+        raise ValueError("coefficients must be a vector or a (batch, N) matrix")
+    dev = device()
+    if cplx:
+        if is_torch:
+            t = arr.to(dev)
+            t = t.reshape(-1, t.shape[-1])
+            both = torch.stack([t.real, t.imag], dim=1).reshape(-1, t.shape[-1])
+            realt = both.to(torch.float64).contiguous()
+        else:
+            a2 = arr.reshape(-1, arr.shape[-1])
+            both = np.stack([a2.real, a2.imag], axis=1).reshape(-1, arr.shape[-1])
+            realt = to_dev_f64(both, dev)
+    else:
+        realt = to_dev_f64(arr.reshape(-1, arr.shape[-1]) if not is_torch else arr.reshape(-1, arr.shape[-1]), dev)
+    return realt, dict(torch=is_torch, complex=cplx, one=one)
+
+
+def from_real_batch(F, meta):
+    """Inverse of as_real_batch for the (B', n_out) result tensor."""
+    if meta["complex"]:
+        F = F.reshape(-1, 2, F.shape[-1])
+        F = torch.complex(F[:, 0], F[:, 1])
+    if meta["one"]:
+        F = F[0]
+    if meta["torch"]:
+        return F
+    return F.cpu().numpy()

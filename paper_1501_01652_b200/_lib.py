@@ -1,0 +1,119 @@
+"""ctypes binding of libfhtb200.so (C ABI in include/fhtb200.h).
+
+The product path has no CPU fallback: if the shared library (or a CUDA
+device) is missing, every numerical entry point raises.
+"""
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libfhtb200.so")
+
+FHTB_OK, FHTB_EINVAL, FHTB_ECUDA, FHTB_ENONFINITE, FHTB_ECONVERGE = 0, 1, 2, 3, 4
+FHTB_DCT1, FHTB_DST1 = 0, 1
+FHTB_FAR, FHTB_NEAR, FHTB_OVERWRITE = 1, 2, 4
+
+i32, i64, f64, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+P_i64 = ctypes.POINTER(ctypes.c_int64)
+P_i32 = ctypes.POINTER(ctypes.c_int32)
+P_f64 = ctypes.POINTER(ctypes.c_double)
+
+
+class GridDesc(ctypes.Structure):
+    _fields_ = [("L", i64), ("gamma", f64), ("m_terms", i32), ("n_blocks", i32),
+                ("blocks", P_i64), ("n_segments", i32), ("segments", P_i64),
+                ("row_first", i64), ("row_stride", i64), ("n_out", i64),
+                ("n_data_cols", i64), ("n_orders", i32), ("orders", P_i32)]
+
+
+class Request(ctypes.Structure):
+    _fields_ = [("vec", i32), ("n_terms", i32), ("orders", P_i32), ("weights", P_f64),
+                ("col_lo", i64), ("pre_a", vp), ("pre_a_pow", i32), ("pre_b", vp),
+                ("pre_b_pow", i32), ("post_r_pow", i32), ("post_e", vp), ("post_e_pow", i32)]
+
+
+class DirectDesc(ctypes.Structure):
+    _fields_ = [("n_rows", i64), ("row_val", vp), ("n_cols", i64), ("col_val", vp),
+                ("n_data_cols", i64), ("r_scale", f64), ("n_orders", i32), ("orders", P_i32)]
+
+
+EXPORTS = {
+    "fhtb_abi_version": (i32, []),
+    "fhtb_last_error": (ctypes.c_char_p, []),
+    "fhtb_init": (i32, []),
+    "fhtb_set_option": (i32, [ctypes.c_char_p, i64]),
+    "fhtb_bessel_j": (i32, [i32, vp, i64, vp, vp]),
+    "fhtb_bessel_j_multi": (i32, [i32, vp, i64, vp, vp]),
+    "fhtb_hankel_asy_eval": (i32, [i32, i32, vp, i64, vp, vp]),
+    "fhtb_taylor_eval": (i32, [i32, i32, vp, i64, vp, vp]),
+    "fhtb_roots_j0": (i32, [i64, vp, vp, P_f64, vp]),
+    "fhtb_fft": (i32, [i64, i32, vp, vp, i64, vp]),
+    "fhtb_trig_workspace": (ctypes.c_size_t, [i32, i64, i64]),
+    "fhtb_trig_apply": (i32, [i32, i64, vp, i64, vp, vp, ctypes.c_size_t, vp]),
+    "fhtb_grid_create": (i32, [ctypes.POINTER(GridDesc), ctypes.POINTER(vp)]),
+    "fhtb_grid_destroy": (None, [vp]),
+    "fhtb_apply_workspace": (ctypes.c_size_t, [vp, i32, i32, i32]),
+    "fhtb_apply": (i32, [vp, ctypes.POINTER(Request), i32, vp, i64, i32, vp, i64, i32, vp,
+                         ctypes.c_size_t, vp]),
+    "fhtb_direct_workspace": (ctypes.c_size_t, [ctypes.POINTER(DirectDesc), i32, i32]),
+    "fhtb_direct_apply": (i32, [ctypes.POINTER(DirectDesc), ctypes.POINTER(Request), i32, vp,
+                                i64, i32, vp, i64, i32, vp, ctypes.c_size_t, vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path=LIB_PATH):
+    """Load the CUDA library; raise if it is missing (no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise RuntimeError(
+                    "libfhtb200.so not found at %s; build it with "
+                    "`python -m paper_1501_01652_b200.build` (no CPU fallback exists)" % path)
+            lib = ctypes.CDLL(path)
+            for name, (res, args) in EXPORTS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+class FhtbError(RuntimeError):
+    pass
+
+
+def check(code):
+    """Map an ABI status code to the reference's exception types."""
+    if code == FHTB_OK:
+        return
+    msg = load().fhtb_last_error().decode(errors="replace")
+    if code == FHTB_EINVAL:
+        raise ValueError(msg)
+    raise FhtbError(msg)
+
+
+def call(name, *args):
+    check(getattr(load(), name)(*args))
+
+
+def i64_array(vals):
+    a = np.ascontiguousarray(np.asarray(vals, dtype=np.int64).ravel())
+    return a, a.ctypes.data_as(P_i64)
+
+
+def i32_array(vals):
+    a = np.ascontiguousarray(np.asarray(vals, dtype=np.int32).ravel())
+    return a, a.ctypes.data_as(P_i32)
+
+
+def f64_array(vals):
+    a = np.ascontiguousarray(np.asarray(vals, dtype=np.float64).ravel())
+    return a, a.ctypes.data_as(P_f64)

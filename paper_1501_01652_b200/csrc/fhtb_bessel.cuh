@@ -1,0 +1,147 @@
+// fhtb_bessel.cuh -- fp64 J_nu(z) evaluators for integer nu >= 0, z >= 0.
+//
+// Same three-branch method as the reference point evaluator
+// (bessel.py:232-260): 10-term Taylor series below t_{nu,10}(2^-52)
+// (bessel.py:133-146), 10-pair Hankel asymptotic expansion above
+// s_{nu,10}(2^-52) (bessel.py:72-91), Miller's backward recurrence with the
+// J0 + 2 sum J_2k = 1 normalisation in between (bessel.py:197-229).
+// Differences (rounding level only): the Miller start order is chosen per
+// element instead of from the tile maximum, and the Hankel phase is formed by
+// rotating (cos z, sin z) by the exact octant angle (2nu+1)pi/4.
+//
+// jn_all(): one Miller sweep that yields J_0..J_omax together (used by the
+// multi-order near field of the Fourier-Bessel / DHT engines, where the
+// reference re-runs Miller once per order, schlomilch.py:512-523).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace fhtb {
+
+constexpr int kAsyPairs = 10;      // bessel.py:40  _ASY_TERMS
+constexpr int kTaylorTerms = 10;   // bessel.py:39  _TAYLOR_TERMS
+constexpr int kMaxOrder = 63;      // orders supported by the device tables
+
+// Per-order constants, filled on the host (fhtb_host.cpp).
+struct JOrder {
+  double tlo;               // taylor_cutoff(nu, 10, 2^-52)
+  double shi;               // asy_cutoff(nu, 10, 2^-52)
+  double inv_fact;          // 1 / nu!
+  double cphi, sphi;        // cos, sin of (2nu+1) pi/4
+  double ae[kAsyPairs];     // (-1)^m a_{2m}(nu)
+  double ao[kAsyPairs];     // (-1)^m a_{2m+1}(nu)
+};
+
+#define FHTB_SQRT_2_OVER_PI 0.79788456080286535588
+
+__device__ __forceinline__ double jn_taylor(int nu, double z, const JOrder& c) {
+  const double h = 0.5 * z;
+  double term = c.inv_fact;
+  for (int i = 0; i < nu; ++i) term *= h;
+  double acc = term;
+  const double hh = h * h;
+#pragma unroll
+  for (int t = 1; t < kTaylorTerms; ++t) {
+    term = -term * hh / (double)(t * (t + nu));
+    acc += term;
+  }
+  return acc;
+}
+
+// Hankel expansion given (cos z, sin z).
+__device__ __forceinline__ double jn_hankel_cs(double z, double cz, double sz, const JOrder& c) {
+  const double w = 1.0 / (z * z);
+  double pe = c.ae[kAsyPairs - 1], po = c.ao[kAsyPairs - 1];
+#pragma unroll
+  for (int m = kAsyPairs - 2; m >= 0; --m) {
+    pe = fma(pe, w, c.ae[m]);
+    po = fma(po, w, c.ao[m]);
+  }
+  const double cm = cz * c.cphi + sz * c.sphi;   // cos(z - phi)
+  const double sm = sz * c.cphi - cz * c.sphi;   // sin(z - phi)
+  return FHTB_SQRT_2_OVER_PI * rsqrt(z) * (cm * pe - sm * po / z);
+}
+
+__device__ __forceinline__ double jn_hankel(double z, const JOrder& c) {
+  double s, co;
+  sincos(z, &s, &co);
+  return jn_hankel_cs(z, co, s, c);
+}
+
+__device__ __forceinline__ int miller_start(double b) {
+  return (int)ceil(b + 10.0 + 11.0 * cbrt(b));
+}
+
+// Miller for a single order nu, mid-range z > 0.
+__device__ __forceinline__ double jn_miller(int nu, double z) {
+  const double b = fmax((double)nu, z);
+  const int k0 = miller_start(b);
+  const double rz = 1.0 / z;
+  double up = 0.0, cur = 1e-30, nrm = 0.0, cap = 0.0;
+  for (int k = k0; k > 0; --k) {
+    const double lo = fma((2.0 * k) * rz, cur, -up);
+    up = cur;
+    cur = lo;
+    const int o = k - 1;
+    if (o == nu) cap = cur;
+    if ((o & 1) == 0) nrm += (o == 0) ? cur : 2.0 * cur;
+    if (fabs(cur) > 1e250) {
+      cur *= 1e-250; up *= 1e-250; nrm *= 1e-250; cap *= 1e-250;
+    }
+  }
+  return cap / nrm;
+}
+
+// J_nu(z), reference dispatch (bessel.py:245-256).
+__device__ __forceinline__ double jn(int nu, double z, const JOrder& c) {
+  if (z <= c.tlo) return jn_taylor(nu, z, c);
+  if (z >= c.shi) return jn_hankel(z, c);
+  return jn_miller(nu, z);
+}
+
+// J_0..J_{omax}(z) into out[] (omax < OMAX).  Branch per element: Taylor is
+// not needed (Miller is accurate for all small z > 0); Hankel per order
+// where z clears that order's cutoff, sharing one sincos.
+template <int OMAX>
+__device__ __forceinline__ void jn_all(int omax, double z, const JOrder* __restrict__ tab,
+                                        double (&out)[OMAX]) {
+  if (z == 0.0) {
+#pragma unroll
+    for (int o = 0; o < OMAX; ++o) out[o] = (o == 0) ? 1.0 : 0.0;
+    return;
+  }
+  if (z >= tab[omax].shi) {
+    double s, co;
+    sincos(z, &s, &co);
+#pragma unroll
+    for (int o = 0; o < OMAX; ++o) out[o] = (o <= omax) ? jn_hankel_cs(z, co, s, tab[o]) : 0.0;
+    return;
+  }
+  const double b = fmax((double)omax, z);
+  const int k0 = miller_start(b);
+  const double rz = 1.0 / z;
+  double up = 0.0, cur = 1e-30, nrm = 0.0;
+#pragma unroll
+  for (int o = 0; o < OMAX; ++o) out[o] = 0.0;
+  for (int k = k0; k > 0; --k) {
+    const double lo = fma((2.0 * k) * rz, cur, -up);
+    up = cur;
+    cur = lo;
+    const int o = k - 1;
+    if (o < OMAX) {
+#pragma unroll
+      for (int q = 0; q < OMAX; ++q)
+        if (q == o) out[q] = cur;
+    }
+    if ((o & 1) == 0) nrm += (o == 0) ? cur : 2.0 * cur;
+    if (fabs(cur) > 1e250) {
+      cur *= 1e-250; up *= 1e-250; nrm *= 1e-250;
+#pragma unroll
+      for (int q = 0; q < OMAX; ++q) out[q] *= 1e-250;
+    }
+  }
+  const double inv = 1.0 / nrm;
+#pragma unroll
+  for (int o = 0; o < OMAX; ++o) out[o] = (o <= omax) ? out[o] * inv : 0.0;
+}
+
+}  // namespace fhtb

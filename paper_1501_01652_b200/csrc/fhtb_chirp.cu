@@ -1,0 +1,520 @@
+// fhtb_chirp.cu -- far field on grids that are not a power of two, or whose
+// output rows are a strided subset (the DHT's padded grid 4N+3 with rows
+// 4k-1, dht.py:158-174), by chirp-z convolution on power-of-two FFTs.
+//
+// For block rows k_j = k0 + s j (j < J; k0 = the grid's first output row so
+// that output ownership is block independent) and block columns
+// n_m = n0 + m (m < Mn), with E(P) = e^{i pi P / (2L)} and all phases reduced
+// in exact integer arithmetic:
+//
+//   sum_m x_m e^{i pi k_j n_m / L}
+//     = E(2 k0 n0 + 2 s j n0 + s j^2) * sum_m [x_m E(2 k0 m + s m^2)] E(-s (j-m)^2)
+//
+// i.e. a linear convolution of length Mn + J - 1 <= Q = 2^logQ computed as
+// IFFT_Q(FFT_Q(a) * H), H = FFT_Q(h) precomputed per block.  Each of the 2M
+// asymptotic terms of a request is one convolution; the column weights,
+// pre-multipliers and in-chirp are applied while loading, the out-chirp, the
+// row weights, order combination and post-multipliers in the epilogue.
+//
+//   pass 1: per column n1 of a = (n1 + Q1 n2), Q2-point FFT over n2, twiddle
+//   pass 2: per column k2, Q1-point FFT over n1, * H, inverse Q1-point FFT,
+//           twiddle, in place
+//   pass 3: per column n1', inverse Q2-point FFT over k2, epilogue
+#include "fhtb_core.cuh"
+#include "fhtb_launch.h"
+
+namespace fhtb {
+
+__device__ __forceinline__ double ipow_c(double x, int p) {
+  double r = 1.0;
+  for (int i = 0; i < p; ++i) r *= x;
+  return r;
+}
+
+__device__ __forceinline__ long long mod4(long long P, long long L4) {
+  long long m = P % L4;
+  return m < 0 ? m + L4 : m;
+}
+
+// e^{i pi P / (2L)}
+__device__ __forceinline__ double2 chirpE(long long P, long long L) { return expi_pi_frac(mod4(P, 4 * L), 2 * L); }
+
+__device__ __forceinline__ double2 qtw_s(const FarArgs& a, long long m, int sign) {
+  const int lo = (int)(m & ((1LL << a.qbits) - 1));
+  const long long hi = m >> a.qbits;
+  double2 w = __ldg(a.qlo + lo);
+  if (hi) w = cmul(w, __ldg(a.qhi + hi));
+  return sign > 0 ? w : cconj(w);
+}
+
+// ------------------------------------------------------------------ pass 1
+template <int N2, int E, int W>
+__global__ void __launch_bounds__(W * (N2 / E))
+chirp_pass1_kernel(FarArgs a) {
+  constexpr int T = N2 / E;
+  constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
+  constexpr int NP = N2 + PAD;
+  extern __shared__ double2 sm2[];
+  const int tid = threadIdx.x, w = tid % W, tt = tid / W;
+  const int Q1 = a.L1;
+  const long long Q = (long long)Q1 * N2;
+  const long long n1 = (long long)blockIdx.x * W + w;
+  const int ul = blockIdx.y;
+  const UnitDesc U = a.units[a.u0 + ul];
+  const ReqDesc& R = a.reqs[U.req];
+  const BlockDesc& B = a.blocks[U.block];
+  const long long cA = max(max(B.c0, R.col_lo), 1LL);
+  const long long cB = min(B.c1, min(a.n_data_cols + 1, a.L + 1));
+  const long long k0 = a.first, s = a.stride, n0 = B.c0, L = a.L;
+  double br[E], bi[E], iw[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const long long m = n1 + (long long)Q1 * (tt + T * e);
+    const long long n = n0 + m;
+    br[e] = bi[e] = iw[e] = 0.0;
+    if (n >= cA && n < cB) {
+      double x = a.C[(long long)R.vec * a.ldc + (n - 1)];
+      if (R.preA) x *= ipow_c(R.preA[n - 1], R.pa);
+      if (R.preB) x *= ipow_c(R.preB[n - 1], R.pb);
+      const double om = ((double)n + a.gamma) * 3.141592653589793;
+      iw[e] = 1.0 / om;
+      const double v = x * (1.0 / sqrt(om));
+      const double2 c = chirpE(2 * k0 * m + s * ((m * m) % (4 * L)), L);
+      br[e] = v * c.x;
+      bi[e] = v * c.y;
+    }
+  }
+  double2* sm = sm2 + w * NP;
+  const double2* tw = a.tw + (N2 - 2);
+  const int nterm = 2 * a.M;
+  for (int i = 0; i < nterm; ++i) {
+    double2 z[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      z[e] = make_double2(br[e], bi[e]);
+      br[e] *= iw[e];
+      bi[e] *= iw[e];
+    }
+    __syncthreads();
+    block_fft<N2, E, -1>(z, sm, tt, tw);
+    double2* G = a.G + (long long)(ul * nterm + i) * Q;
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const int k2 = fft_out_index<N2, E>(tt, q);
+      G[(long long)k2 * Q1 + n1] = cmul(z[q], qtw_s(a, n1 * k2, -1));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ pass 2
+template <int N1, int E>
+__global__ void __launch_bounds__(N1 / E)
+chirp_pass2_kernel(FarArgs a) {
+  constexpr int T = N1 / E;
+  using Sh = FftShape<N1, E>;
+  constexpr int RL = Sh::RL;
+  extern __shared__ double2 sm2[];
+  const int tt = threadIdx.x;
+  const int k2 = blockIdx.x;
+  const int ul = blockIdx.y;
+  const int Q2 = a.L2;
+  const long long Q = (long long)N1 * Q2;
+  const UnitDesc U = a.units[a.u0 + ul];
+  const BlockDesc& B = a.blocks[U.block];
+  const double2* __restrict__ H = B.H;
+  const double2* tw = a.tw + (N1 - 2);
+  const int nterm = 2 * a.M;
+  for (int i = 0; i < nterm; ++i) {
+    double2* row = a.G + (long long)(ul * nterm + i) * Q + (long long)k2 * N1;
+    double2 z[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) z[e] = row[tt + T * e];
+    __syncthreads();
+    block_fft<N1, E, -1>(z, sm2, tt, tw);
+    double2 y[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const int k1 = fft_out_index<N1, E>(tt, q);
+      const double2 h = __ldg(H + k2 + (long long)Q2 * k1);
+      y[(q / RL) + (q % RL) * (E / RL)] = cmul(z[q], h);
+    }
+    __syncthreads();
+    block_fft<N1, E, 1>(y, sm2, tt, tw);
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const int n1 = fft_out_index<N1, E>(tt, q);
+      row[n1] = cmul(y[q], qtw_s(a, (long long)n1 * k2, 1));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ pass 3
+// One CTA per (column group, unit): all 2M terms of the unit are reduced in
+// registers and written as a per-unit partial row part[unit][j]; the
+// partials of one vector are summed in unit order by chirp_reduce_kernel.
+template <int N2, int E, int W>
+__global__ void __launch_bounds__(W * (N2 / E))
+chirp_pass3_kernel(FarArgs a) {
+  constexpr int T = N2 / E;
+  constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
+  constexpr int NP = N2 + PAD;
+  extern __shared__ double2 sm2[];
+  const int tid = threadIdx.x, w = tid % W, tt = tid / W;
+  const int Q1 = a.L1;
+  const long long Q = (long long)Q1 * N2;
+  const long long n1 = (long long)blockIdx.x * W + w;
+  const int ul = blockIdx.y;
+  const long long L = a.L, k0 = a.first, s = a.stride;
+  const double invQ = 1.0 / (double)Q;
+  const UnitDesc U = a.units[a.u0 + ul];
+  const ReqDesc& R = a.reqs[U.req];
+  const BlockDesc& B = a.blocks[U.block];
+  const long long n0 = B.c0;
+  double acc[E], rp[E], ir[E];
+  double2 oc[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    const long long j = n1 + (long long)Q1 * fft_out_index<N2, E>(tt, q);
+    const long long k = k0 + s * j;
+    acc[q] = rp[q] = ir[q] = 0.0;
+    oc[q] = make_double2(0.0, 0.0);
+    if (j < B.J && k >= B.r0 && k < B.r1 && k <= L) {
+      const double irk = a.Ld / (double)k;
+      double post = 1.0;
+      if (R.pr) post = ipow_c((double)k / a.Ld, R.pr);
+      if (R.post_e && R.pe) post *= ipow_c(R.post_e[j], R.pe);
+      ir[q] = irk;
+      rp[q] = post * sqrt(irk);
+      const long long P = 2 * k0 * n0 + 2 * s * j * n0 + s * ((j * j) % (4 * L));
+      const double2 c = chirpE(P, L);
+      oc[q] = make_double2(c.x * invQ, c.y * invQ);
+    }
+  }
+  double thc[E], ths[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    thc[q] = 1.0;
+    ths[q] = 0.0;
+    if (a.gamma != 0.0 && rp[q] != 0.0) {
+      const long long j = n1 + (long long)Q1 * fft_out_index<N2, E>(tt, q);
+      sincos(-a.gamma * (double)(k0 + s * j) * a.pi_over_L, &ths[q], &thc[q]);
+    }
+  }
+  double2* sm = sm2 + w * NP;
+  const double2* tw = a.tw + (N2 - 2);
+  const int nterm = 2 * a.M;
+  for (int i = 0; i < nterm; ++i) {
+    const double2* G = a.G + (long long)(ul * nterm + i) * Q;
+    double2 z[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) z[e] = G[(long long)(tt + T * e) * Q1 + n1];
+    __syncthreads();
+    block_fft<N2, E, 1>(z, sm, tt, tw);
+    const double ac = R.ac[i], as_ = R.as[i], bc = R.bc[i], bs = R.bs[i];
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      if (rp[q] == 0.0) continue;
+      const double2 Y = cmul(z[q], oc[q]);
+      const double A = ac * thc[q] + as_ * ths[q], Bv = bc * thc[q] + bs * ths[q];
+      acc[q] += rp[q] * (A * Y.x + Bv * Y.y);
+      rp[q] *= ir[q];
+    }
+  }
+  double* part = a.part + (long long)ul * a.part_stride;
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    const long long j = n1 + (long long)Q1 * fft_out_index<N2, E>(tt, q);
+    if (j < a.n_out && ir[q] != 0.0) part[j] = acc[q];
+  }
+}
+
+// F[vec][j] += sum over the chunk's units of that vector (unit order).
+__global__ void chirp_reduce_kernel(FarArgs a, int n_units) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= a.n_out) return;
+  int u = 0;
+  while (u < n_units) {
+    const int vec = a.units[a.u0 + u].vec;
+    double s = 0.0;
+    while (u < n_units && a.units[a.u0 + u].vec == vec) {
+      s += a.part[(long long)u * a.part_stride + j];
+      ++u;
+    }
+    a.F[(long long)vec * a.ldf + j] += s;
+  }
+}
+
+cudaError_t launch_chirp_reduce(const FarArgs& a, int n_units, cudaStream_t st) {
+  const long long b = (a.n_out + 255) / 256;
+  chirp_reduce_kernel<<<(unsigned)b, 256, 0, st>>>(a, n_units);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------- plain FFT passes (filters)
+// out[k2*Q1 + n1] = e^{S 2 pi i n1 k2/Q} * FFT_{N2}(in[n1 + Q1 n2])
+template <int N2, int E, int W, int S>
+__global__ void __launch_bounds__(W * (N2 / E))
+plain_pass1_kernel(const double2* __restrict__ in, double2* __restrict__ out, FarArgs a) {
+  constexpr int T = N2 / E;
+  constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
+  constexpr int NP = N2 + PAD;
+  extern __shared__ double2 sm2[];
+  const int tid = threadIdx.x, w = tid % W, tt = tid / W;
+  const int Q1 = a.L1;
+  const long long n1 = (long long)blockIdx.x * W + w;
+  double2 z[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) z[e] = in[n1 + (long long)Q1 * (tt + T * e)];
+  block_fft<N2, E, S>(z, sm2 + w * NP, tt, a.tw + (N2 - 2));
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    const int k2 = fft_out_index<N2, E>(tt, q);
+    out[(long long)k2 * Q1 + n1] = cmul(z[q], qtw_s(a, n1 * k2, S));
+  }
+}
+
+// out[k2 + Q2 k1] = FFT_{N1}(in[k2*N1 + n1])
+template <int N1, int E, int S>
+__global__ void __launch_bounds__(N1 / E)
+plain_pass2_kernel(const double2* __restrict__ in, double2* __restrict__ out, FarArgs a) {
+  constexpr int T = N1 / E;
+  extern __shared__ double2 sm2[];
+  const int tt = threadIdx.x, k2 = blockIdx.x, Q2 = a.L2;
+  double2 z[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) z[e] = in[(long long)k2 * N1 + tt + T * e];
+  block_fft<N1, E, S>(z, sm2, tt, a.tw + (N1 - 2));
+#pragma unroll
+  for (int q = 0; q < E; ++q) out[k2 + (long long)Q2 * fft_out_index<N1, E>(tt, q)] = z[q];
+}
+
+// h[d mod Q] = E(-s d^2) for d in [-(Mn-1), J-1], else 0
+__global__ void chirp_filter_kernel(double2* h, long long Q, long long Mn, long long J, long long s, long long L) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < Q; i += (long long)gridDim.x * blockDim.x) {
+    long long d = i <= J - 1 ? i : i - Q;   // i in [0, J) -> d = i ; i in [Q-(Mn-1), Q) -> d = i - Q
+    double2 v = make_double2(0.0, 0.0);
+    if (i < J || (i >= Q - (Mn - 1))) {
+      const long long d2 = (d * d) % (4 * L);
+      v = chirpE(-s * d2, L);
+    }
+    h[i] = v;
+  }
+}
+
+// ------------------------------------------------------------ DCT-I/DST-I
+// One CTA per row, Q <= 8192: out[k] = Re/Im sum_{m<n} v_m e^{i pi (k0+k)(n0+m)/L}
+template <int N, int E>
+__global__ void __launch_bounds__(N / E)
+trig_kernel(int kind, long long n, long long L, long long k0, long long n0, const double* __restrict__ v,
+            double* __restrict__ out, const double2* __restrict__ H, const double2* __restrict__ tw_pool) {
+  constexpr int T = N / E;
+  using Sh = FftShape<N, E>;
+  constexpr int RL = Sh::RL;
+  extern __shared__ double2 sm2[];
+  const int tt = threadIdx.x;
+  const double* x = v + (long long)blockIdx.x * n;
+  double2 z[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const long long m = tt + T * e;
+    z[e] = make_double2(0.0, 0.0);
+    if (m < n) {
+      const double2 c = chirpE(2 * k0 * m + ((m * m) % (4 * L)), L);
+      z[e] = make_double2(x[m] * c.x, x[m] * c.y);
+    }
+  }
+  const double2* tw = tw_pool + (N - 2);
+  block_fft<N, E, -1>(z, sm2, tt, tw);
+  double2 y[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) y[(q / RL) + (q % RL) * (E / RL)] = cmul(z[q], __ldg(H + fft_out_index<N, E>(tt, q)));
+  __syncthreads();
+  block_fft<N, E, 1>(y, sm2, tt, tw);
+  double* o = out + (long long)blockIdx.x * n;
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    const long long j = fft_out_index<N, E>(tt, q);
+    if (j < n) {
+      const long long P = 2 * k0 * n0 + 2 * j * n0 + ((j * j) % (4 * L));
+      const double2 c = chirpE(P, L);
+      const double2 Y = cmul(y[q], c);
+      o[j] = (kind == 0 ? Y.x : Y.y) / (double)N;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- launch
+static int pick_w(int N2) {
+  int T = N2 >= 8 ? N2 / 8 : 1;
+  int w = 256 / T;
+  if (w < 1) w = 1;
+  if (w > 8) w = 8;
+  return w;
+}
+
+template <int N2, int W>
+static cudaError_t c1_w(const FarArgs& a, int n_units, cudaStream_t st) {
+  constexpr int E = N2 >= 8 ? 8 : N2;
+  constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
+  const int smem = W * (N2 + PAD) * 16;
+  auto k = chirp_pass1_kernel<N2, E, W>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k<<<dim3(a.L1 / W, n_units), W * (N2 / E), smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int N2, int W>
+static cudaError_t c3_w(const FarArgs& a, int n_ranges, cudaStream_t st) {
+  constexpr int E = N2 >= 8 ? 8 : N2;
+  constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
+  const int smem = W * (N2 + PAD) * 16;
+  auto k = chirp_pass3_kernel<N2, E, W>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k<<<dim3(a.L1 / W, n_ranges), W * (N2 / E), smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int N2, int W, int S>
+static cudaError_t pp1_w(const double2* in, double2* out, const FarArgs& a, cudaStream_t st) {
+  constexpr int E = N2 >= 8 ? 8 : N2;
+  constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
+  const int smem = W * (N2 + PAD) * 16;
+  auto k = plain_pass1_kernel<N2, E, W, S>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k<<<dim3(a.L1 / W), W * (N2 / E), smem, st>>>(in, out, a);
+  return cudaGetLastError();
+}
+
+// W must divide L1 (Q1); choose the largest power of two <= min(cap, Q1).
+#define FHTB_W_DISPATCH(FN, N2, ...)                                             \
+  do {                                                                           \
+    int w_ = pick_w(N2);                                                         \
+    while (w_ > a.L1) w_ >>= 1;                                                  \
+    switch (w_) {                                                                \
+      case 8: return FN<N2, 8>(__VA_ARGS__);                                     \
+      case 4: return FN<N2, 4>(__VA_ARGS__);                                     \
+      case 2: return FN<N2, 2>(__VA_ARGS__);                                     \
+      default: return FN<N2, 1>(__VA_ARGS__);                                    \
+    }                                                                            \
+  } while (0)
+
+#define FHTB_SIZE_SWITCH(LOG, MACRO)                                             \
+  switch (LOG) {                                                                 \
+    case 1: MACRO(2); case 2: MACRO(4); case 3: MACRO(8); case 4: MACRO(16);     \
+    case 5: MACRO(32); case 6: MACRO(64); case 7: MACRO(128); case 8: MACRO(256);\
+    case 9: MACRO(512); case 10: MACRO(1024); case 11: MACRO(2048);              \
+    case 12: MACRO(4096); case 13: MACRO(8192);                                  \
+  }
+
+cudaError_t launch_chirp_pass1(const FarArgs& a, int logN2, int n_units, cudaStream_t st) {
+#define M1(N) FHTB_W_DISPATCH(c1_w, N, a, n_units, st)
+  FHTB_SIZE_SWITCH(logN2, M1)
+#undef M1
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_chirp_pass3(const FarArgs& a, int logN2, int n_ranges, cudaStream_t st) {
+#define M3(N) FHTB_W_DISPATCH(c3_w, N, a, n_ranges, st)
+  FHTB_SIZE_SWITCH(logN2, M3)
+#undef M3
+  return cudaErrorInvalidValue;
+}
+
+template <int N1>
+static cudaError_t c2_t(const FarArgs& a, int n_units, cudaStream_t st) {
+  constexpr int E = N1 >= 8 ? 8 : N1;
+  const int smem = N1 * 16;
+  auto k = chirp_pass2_kernel<N1, E>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k<<<dim3(a.L2, n_units), N1 / E, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chirp_pass2(const FarArgs& a, int logN1, int n_units, cudaStream_t st) {
+#define M2(N) return c2_t<N>(a, n_units, st);
+  FHTB_SIZE_SWITCH(logN1, M2)
+#undef M2
+  return cudaErrorInvalidValue;
+}
+
+template <int N1, int S>
+static cudaError_t pp2_t(const double2* in, double2* out, const FarArgs& a, cudaStream_t st) {
+  constexpr int E = N1 >= 8 ? 8 : N1;
+  const int smem = N1 * 16;
+  auto k = plain_pass2_kernel<N1, E, S>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k<<<dim3(a.L2), N1 / E, smem, st>>>(in, out, a);
+  return cudaGetLastError();
+}
+
+// Forward (sign -1) FFT of length Q = L1*L2 of a device vector, out-of-place
+// through `tmp`.  Used to build the chirp filter spectra.
+cudaError_t launch_plain_fft(const FarArgs& a, int logN1, int logN2, const double2* in, double2* tmp,
+                             double2* out, cudaStream_t st) {
+  cudaError_t e = cudaErrorInvalidValue;
+#define PP1(N) { FHTB_W_DISPATCH_P1(N); }
+#define FHTB_W_DISPATCH_P1(N)                                                    \
+  do {                                                                           \
+    int w_ = pick_w(N);                                                          \
+    while (w_ > a.L1) w_ >>= 1;                                                  \
+    switch (w_) {                                                                \
+      case 8: e = pp1_w<N, 8, -1>(in, tmp, a, st); break;                        \
+      case 4: e = pp1_w<N, 4, -1>(in, tmp, a, st); break;                        \
+      case 2: e = pp1_w<N, 2, -1>(in, tmp, a, st); break;                        \
+      default: e = pp1_w<N, 1, -1>(in, tmp, a, st); break;                       \
+    }                                                                            \
+  } while (0); break;
+  switch (logN2) {
+    case 1: PP1(2) case 2: PP1(4) case 3: PP1(8) case 4: PP1(16) case 5: PP1(32) case 6: PP1(64)
+    case 7: PP1(128) case 8: PP1(256) case 9: PP1(512) case 10: PP1(1024) case 11: PP1(2048)
+    case 12: PP1(4096) case 13: PP1(8192)
+    default: return cudaErrorInvalidValue;
+  }
+#undef PP1
+#undef FHTB_W_DISPATCH_P1
+  if (e != cudaSuccess) return e;
+#define PP2(N) e = pp2_t<N, -1>(tmp, out, a, st); break;
+  switch (logN1) {
+    case 1: PP2(2) case 2: PP2(4) case 3: PP2(8) case 4: PP2(16) case 5: PP2(32) case 6: PP2(64)
+    case 7: PP2(128) case 8: PP2(256) case 9: PP2(512) case 10: PP2(1024) case 11: PP2(2048)
+    case 12: PP2(4096) case 13: PP2(8192)
+    default: return cudaErrorInvalidValue;
+  }
+#undef PP2
+  return e;
+}
+
+cudaError_t launch_chirp_filter(double2* h, long long Q, long long Mn, long long J, long long s, long long L,
+                                cudaStream_t st) {
+  long long b = (Q + 255) / 256;
+  if (b > 148 * 64) b = 148 * 64;
+  chirp_filter_kernel<<<(int)b, 256, 0, st>>>(h, Q, Mn, J, s, L);
+  return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t trig_t(int kind, long long n, long long L, long long k0, long long n0, const double* v,
+                          double* out, long long batch, const double2* H, const double2* tw, cudaStream_t st) {
+  constexpr int E = N >= 16 ? 16 : N;
+  const int smem = N * 16;
+  auto k = trig_kernel<N, E>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k<<<(unsigned)batch, N / E, smem, st>>>(kind, n, L, k0, n0, v, out, H, tw);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trig(int kind, int logQ, long long n, long long L, long long k0, long long n0, const double* v,
+                        double* out, long long batch, const double2* H, const double2* tw, cudaStream_t st) {
+#define TT(N) return trig_t<N>(kind, n, L, k0, n0, v, out, batch, H, tw, st);
+  FHTB_SIZE_SWITCH(logQ, TT)
+#undef TT
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace fhtb

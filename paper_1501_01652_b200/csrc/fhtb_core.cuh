@@ -1,0 +1,226 @@
+// fhtb_core.cuh -- device building blocks shared by every kernel of libfhtb200.
+//
+//  * complex helpers on double2
+//  * exact-phase unit roots  e^{i pi P / D}  for integer P, D
+//  * register/shared-memory Stockham FFT (radix 16/8/4/2, fp64) used by the
+//    DCT-I/DST-I far-field kernels (reference: trig.py:59-77 rfft embeddings,
+//    schlomilch.py:301-329 block application)
+//
+// Everything here is header-only and compiled for sm_100a.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fhtb {
+
+// ---------------------------------------------------------------- complex
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * (S*i), S = +1 or -1
+template <int S> __device__ __forceinline__ double2 cmul_i(double2 a) {
+  return S > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+// e^{i pi P / D} for integer P (any sign) and D > 0, with the argument reduced
+// in exact integer arithmetic to [0, 1/2) before sincospi, so the phase
+// error stays below one ulp even for D that is not a power of two.
+__device__ __forceinline__ double2 expi_pi_frac(long long P, long long D) {
+  long long m = P % (2 * D);
+  if (m < 0) m += 2 * D;
+  double sgn = 1.0;
+  if (m >= D) { m -= D; sgn = -1.0; }
+  // angle pi*m/D in [0, pi)
+  double s, c;
+  if (2 * m >= D) {
+    // pi*m/D = pi/2 + pi*(2m-D)/(2D);  e^{i(pi/2+x)} = i e^{ix}
+    sincospi((double)(2 * m - D) / (double)(2 * D), &s, &c);
+    return make_double2(-s * sgn, c * sgn);
+  }
+  sincospi((double)m / (double)D, &s, &c);
+  return make_double2(c * sgn, s * sgn);
+}
+
+// ------------------------------------------------------------ small DFTs
+// In-place DFT of R consecutive registers, X_k = sum_n a_n w^{nk},
+// w = e^{S 2 pi i / R}.
+template <int R, int S> struct Dft;
+
+template <int S> struct Dft<1, S> {
+  static __device__ __forceinline__ void run(double2*) {}
+};
+
+template <int S> struct Dft<2, S> {
+  static __device__ __forceinline__ void run(double2* v) {
+    double2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  }
+};
+
+template <int S> struct Dft<4, S> {
+  static __device__ __forceinline__ void run(double2* v) {
+    double2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+    double2 t2 = cadd(v[1], v[3]), t3 = cmul_i<S>(csub(v[1], v[3]));
+    v[0] = cadd(t0, t2);
+    v[2] = csub(t0, t2);
+    v[1] = cadd(t1, t3);
+    v[3] = csub(t1, t3);
+  }
+};
+
+#define FHTB_SQRT1_2 0.70710678118654752440
+#define FHTB_COS_PI8 0.92387953251128675613
+#define FHTB_SIN_PI8 0.38268343236508977173
+
+// w8 = (1 + S i)/sqrt2,  w8^3 = (-1 + S i)/sqrt2
+template <int S> __device__ __forceinline__ double2 mul_w8(double2 a) {
+  return make_double2((a.x - S * a.y) * FHTB_SQRT1_2, (a.y + S * a.x) * FHTB_SQRT1_2);
+}
+template <int S> __device__ __forceinline__ double2 mul_w8_3(double2 a) {
+  return make_double2((-a.x - S * a.y) * FHTB_SQRT1_2, (-a.y + S * a.x) * FHTB_SQRT1_2);
+}
+
+template <int S> struct Dft<8, S> {
+  static __device__ __forceinline__ void run(double2* v) {
+    double2 e[4] = {v[0], v[2], v[4], v[6]};
+    double2 o[4] = {v[1], v[3], v[5], v[7]};
+    Dft<4, S>::run(e);
+    Dft<4, S>::run(o);
+    o[1] = mul_w8<S>(o[1]);
+    o[2] = cmul_i<S>(o[2]);
+    o[3] = mul_w8_3<S>(o[3]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = cadd(e[k], o[k]);
+      v[k + 4] = csub(e[k], o[k]);
+    }
+  }
+};
+
+template <int S> struct Dft<16, S> {
+  static __device__ __forceinline__ void run(double2* v) {
+    double2 e[8], o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { e[k] = v[2 * k]; o[k] = v[2 * k + 1]; }
+    Dft<8, S>::run(e);
+    Dft<8, S>::run(o);
+    const double c1 = FHTB_COS_PI8, s1 = FHTB_SIN_PI8;
+    o[1] = cmul(o[1], make_double2(c1, S * s1));
+    o[2] = mul_w8<S>(o[2]);
+    o[3] = cmul(o[3], make_double2(s1, S * c1));
+    o[4] = cmul_i<S>(o[4]);
+    o[5] = cmul(o[5], make_double2(-s1, S * c1));
+    o[6] = mul_w8_3<S>(o[6]);
+    o[7] = cmul(o[7], make_double2(-c1, S * s1));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v[k] = cadd(e[k], o[k]);
+      v[k + 8] = csub(e[k], o[k]);
+    }
+  }
+};
+
+// ----------------------------------------------------- block Stockham FFT
+//
+// An N-point FFT executed by T threads, each holding E = N/T points in
+// registers.  Input layout: thread t holds x[t + T*e], e < E.  Output
+// layout: slot s = b*RL + r holds X[t + T*b + r*(N/RL)], RL = last radix.
+// Radices: E first, then E repeatedly, last radix = N / E^p.  Shared
+// memory holds N double2 (swizzled, no padding) and is used between passes.
+//
+// tw: table of e^{+2 pi i m / N}, m < N (global, read through L1).
+
+constexpr __host__ __device__ int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n >> 1); }
+
+template <int N, int E> struct FftShape {
+  static constexpr int LOGN = ilog2c(N);
+  static constexpr int LOGE = ilog2c(E);
+  static constexpr int T = N / E;
+  static constexpr int NPASS = (LOGN + LOGE - 1) / LOGE;        // ceil
+  static constexpr int LOGRL = LOGN - (NPASS - 1) * LOGE;         // last radix log
+  static constexpr int RL = 1 << LOGRL;
+};
+
+// XOR swizzle: conflict-free for both unit-stride and stride-E 16-byte accesses.
+template <int LOGE> __device__ __forceinline__ int swz(int i) {
+  return LOGE >= 3 ? (i ^ ((i >> LOGE) & 7)) : i;
+}
+
+template <int S> __device__ __forceinline__ double2 twid(const double2* __restrict__ tw, int m) {
+  double2 w = __ldg(tw + m);
+  return S > 0 ? w : cconj(w);
+}
+
+// One Stockham pass with radix R over the registers of thread t.
+template <int N, int E, int R, int S>
+__device__ __forceinline__ void stockham_mid(double2 (&v)[E], double2* sm, int t, int Ns,
+                                             const double2* __restrict__ tw, bool last) {
+  constexpr int T = N / E;
+  constexpr int NB = E / R;
+  constexpr int STR = N / R;
+  constexpr int LOGE = ilog2c(E);
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int j = t + T * b;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[b * R + r] = sm[swz<LOGE>(j + r * STR)];
+  }
+  const int tstep = N / (Ns * R);
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int j = t + T * b;
+    const int k = j % Ns;
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[b * R + r] = cmul(v[b * R + r], twid<S>(tw, r * k * tstep));
+    Dft<R, S>::run(v + b * R);
+  }
+  if (!last) {
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = t + T * b;
+      const int k = j % Ns;
+      const int d = (j / Ns) * Ns * R + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) sm[swz<LOGE>(d + r * Ns)] = v[b * R + r];
+    }
+    __syncthreads();
+  }
+}
+
+// Full FFT.  Caller guarantees that no other thread of the CTA still reads
+// `sm` from a previous use (a __syncthreads before the call).
+template <int N, int E, int S>
+__device__ __forceinline__ void block_fft(double2 (&v)[E], double2* sm, int t,
+                                          const double2* __restrict__ tw) {
+  using Sh = FftShape<N, E>;
+  constexpr int LOGE = Sh::LOGE;
+  // pass 0: radix E, Ns = 1, inputs already in place, no twiddles
+  Dft<E, S>::run(v);
+  if (Sh::NPASS == 1) return;
+#pragma unroll
+  for (int r = 0; r < E; ++r) sm[swz<LOGE>(t * E + r)] = v[r];
+  __syncthreads();
+  int Ns = E;
+#pragma unroll
+  for (int p = 1; p < Sh::NPASS - 1; ++p) {
+    stockham_mid<N, E, E, S>(v, sm, t, Ns, tw, false);
+    Ns *= E;
+  }
+  stockham_mid<N, E, Sh::RL, S>(v, sm, t, Ns, tw, true);
+}
+
+// Output index held by slot s of thread t after block_fft.
+template <int N, int E>
+__device__ __forceinline__ int fft_out_index(int t, int s) {
+  using Sh = FftShape<N, E>;
+  constexpr int RL = Sh::RL;
+  return t + Sh::T * (s / RL) + (s % RL) * (N / RL);
+}
+
+}  // namespace fhtb

@@ -1,0 +1,322 @@
+// fhtb_far.cu -- far field of the Schlomilch application, direct mode.
+//
+// Reference behaviour (schlomilch.py:301-329, :470-502): for each block and
+// each term i < 2M, u_i = col_w[i] * c on the block columns, C u_i (DCT-I,
+// N+1) and S u_i (DST-I, N-1) via rfft embeddings (trig.py:59-77), then
+// out[rows] += sum_i A_i * C u_i + B_i * S u_i.
+//
+// B200 formulation.  C u + i S u = sum_n u_n e^{+i pi k n / L}, i.e. a
+// length-2L DFT of the zero-padded column vector.  Terms 2p and 2p+1 are
+// real, so they share ONE complex FFT z = u_{2p} + i u_{2p+1}; the two
+// spectra are separated in the epilogue from Z[k] and conj Z[2L-k].
+// The column weights omega_n^{-i-1/2} (and the Fourier-Bessel / DHT
+// pre-multipliers) are generated in registers while loading c (no 2M x N
+// materialisation, cf. schlomilch.py:251-257), and the row weights
+// (L/k)^{i+1/2}, the gamma-shift diagonals cos/sin(theta_k + (2o+1)pi/4)
+// (Remark 1), the order combination (schlomilch.py:280-299) and the
+// post-multipliers r^u / e^u (fourier_bessel.py:240-242, dht.py:167-174) are
+// applied in the epilogue of the last FFT pass, which accumulates all units
+// of one coefficient vector in registers and writes the output once.
+//
+//   one-pass  (2L <= 8192): one CTA per vector, whole FFT in shared memory.
+//   two-pass  (2L  > 8192): Q = 2L = L1*L2 four-step.
+//      pass 1: per column n1, L2-point FFT over n2 (n = n1 + L1 n2), twiddle
+//              e^{2 pi i n1 k2 / Q}, store G[unit][p][k2][n1].
+//      pass 2: per column pair {k2, L2-k2}, L1-point FFTs over n1, then the
+//              fused DCT/DST separation + row epilogue.
+#include "fhtb_core.cuh"
+#include "fhtb_launch.h"
+
+namespace fhtb {
+
+__device__ __forceinline__ double ipow_f(double x, int p) {
+  double r = 1.0;
+  for (int i = 0; i < p; ++i) r *= x;
+  return r;
+}
+
+// Four-step twiddle e^{+2 pi i m / Q}.
+__device__ __forceinline__ double2 qtw(const FarArgs& a, long long m) {
+  const int lo = (int)(m & ((1LL << a.qbits) - 1));
+  const long long hi = m >> a.qbits;
+  double2 w = __ldg(a.qlo + lo);
+  if (hi) w = cmul(w, __ldg(a.qhi + hi));
+  return w;
+}
+
+// Column state of grid column n for request R on block B:
+//   v = x_n * omega_n^{-1/2},  iw = 1/omega_n   (0 outside the block)
+__device__ __forceinline__ void load_col(const FarArgs& a, const ReqDesc& R, long long cA, long long cB,
+                                         long long n, double& v, double& iw) {
+  v = 0.0;
+  iw = 0.0;
+  if (n >= cA && n < cB) {
+    double x = a.C[(long long)R.vec * a.ldc + (n - 1)];
+    if (R.preA) x *= ipow_f(R.preA[n - 1], R.pa);
+    if (R.preB) x *= ipow_f(R.preB[n - 1], R.pb);
+    const double om = ((double)n + a.gamma) * 3.141592653589793;
+    iw = 1.0 / om;
+    v = x * (1.0 / sqrt(om));
+  }
+}
+
+__device__ __forceinline__ void unit_cols(const FarArgs& a, const ReqDesc& R, const BlockDesc& B,
+                                          long long& cA, long long& cB) {
+  cA = max(max(B.c0, R.col_lo), 1LL);
+  cB = min(B.c1, min(a.n_data_cols + 1, a.L + 1));
+}
+
+// ------------------------------------------------------------------ pass 1
+template <int N2, int E, int W>
+__global__ void __launch_bounds__(W * (N2 / E))
+far_pass1_kernel(FarArgs a) {
+  constexpr int T = N2 / E;
+  constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
+  constexpr int NP = N2 + PAD;
+  extern __shared__ double2 sm2[];
+  const int tid = threadIdx.x, w = tid % W, tt = tid / W;
+  const int L1 = a.L1;
+  const long long n1 = (long long)blockIdx.x * W + w;
+  const int ul = blockIdx.y;
+  const UnitDesc U = a.units[a.u0 + ul];
+  const ReqDesc& R = a.reqs[U.req];
+  const BlockDesc& B = a.blocks[U.block];
+  long long cA, cB;
+  unit_cols(a, R, B, cA, cB);
+  double v[E], iw[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) load_col(a, R, cA, cB, n1 + (long long)L1 * (tt + T * e), v[e], iw[e]);
+  double2* sm = sm2 + w * NP;
+  const double2* tw = a.tw + (N2 - 2);
+  for (int p = 0; p < a.M; ++p) {
+    double2 z[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const double im = v[e] * iw[e];
+      z[e] = make_double2(v[e], im);
+      v[e] = im * iw[e];
+    }
+    __syncthreads();
+    block_fft<N2, E, 1>(z, sm, tt, tw);
+    double2* G = a.G + ((long long)(ul * a.M + p) * N2) * L1;
+#pragma unroll
+    for (int s = 0; s < E; ++s) {
+      const int k2 = fft_out_index<N2, E>(tt, s);
+      G[(long long)k2 * L1 + n1] = cmul(z[s], qtw(a, n1 * k2));
+    }
+  }
+}
+
+// --------------------------------------------- pass 2 / one-pass epilogue
+//
+// ONEPASS: L2 == 1, N1 == 2L, one column, input generated from c.
+template <int N1, int E, bool ONEPASS>
+__global__ void __launch_bounds__((ONEPASS ? 1 : 2) * (N1 / E))
+far_pass2_kernel(FarArgs a) {
+  constexpr int T = N1 / E;
+  constexpr int NCOL = ONEPASS ? 1 : 2;
+  constexpr int NT = NCOL * T;
+  constexpr int NQ = E / 2 > 0 ? E / 2 : 1;     // output slots per thread
+  constexpr int HALF = N1 / 2;
+  constexpr int NP = N1 + 4;
+  constexpr int LOGE = ilog2c(E);
+  extern __shared__ double2 sm2[];
+  double2* cs = sm2 + NCOL * NP;               // per-slot (cos theta, sin theta)
+  const int tid = threadIdx.x, h = tid / T, tt = tid % T;
+  const long long L = a.L;
+  const int L2 = a.L2;
+  const int k2a = blockIdx.x, k2b = (L2 - k2a) % L2;
+  const bool selfp = (k2a == k2b);
+  const int myk2 = h == 0 ? k2a : k2b;
+  const int2 vr = a.vranges[blockIdx.y];
+  const double2* tw = a.tw + (N1 - 2);
+
+  // slot geometry
+  long long kq[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int o = tid + NT * q;
+    const int hh = o / HALF, qq = o % HALF;
+    long long k = 0;
+    if (hh < NCOL && !(selfp && hh == 1)) {
+      const int k2 = hh == 0 ? k2a : k2b;
+      const int k1 = (k2 == 0) ? qq + 1 : qq;
+      k = k2 + (long long)L2 * k1;
+      if (k < 1 || k > L) k = 0;
+    }
+    kq[q] = k;
+    double s = 0.0, c = 1.0;
+    if (k && a.gamma != 0.0) sincos(-a.gamma * (double)k * a.pi_over_L, &s, &c);
+    cs[o] = make_double2(c, s);
+  }
+  double acc[NQ], rp[NQ], ir[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+
+  for (int u = vr.x; u < vr.y; ++u) {
+    const UnitDesc U = a.units[u];
+    const ReqDesc& R = a.reqs[U.req];
+    const BlockDesc& B = a.blocks[U.block];
+    // per-slot row weights: rp = post(k) * (L/k)^{1/2} inside the block rows
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const long long k = kq[q];
+      rp[q] = 0.0;
+      ir[q] = 0.0;
+      if (k && k >= B.r0 && k < B.r1) {
+        const double irk = a.Ld / (double)k;
+        const long long j = (k - a.first) / a.stride;
+        double post = 1.0;
+        if (R.pr) post = ipow_f((double)k / a.Ld, R.pr);
+        if (R.post_e && R.pe) post *= ipow_f(R.post_e[j], R.pe);
+        ir[q] = irk;
+        rp[q] = post * sqrt(irk);
+      }
+    }
+    double v[E], iw[E];
+    long long cA = 0, cB = 0;
+    if (ONEPASS) {
+      unit_cols(a, R, B, cA, cB);
+#pragma unroll
+      for (int e = 0; e < E; ++e) load_col(a, R, cA, cB, tt + T * e, v[e], iw[e]);
+    }
+    for (int p = 0; p < a.M; ++p) {
+      double2 z[E];
+      if (ONEPASS) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const double im = v[e] * iw[e];
+          z[e] = make_double2(v[e], im);
+          v[e] = im * iw[e];
+        }
+      } else {
+        const double2* G = a.G + ((long long)((u - a.u0) * a.M + p) * L2 + myk2) * N1;
+#pragma unroll
+        for (int e = 0; e < E; ++e) z[e] = G[tt + T * e];
+      }
+      __syncthreads();
+      block_fft<N1, E, 1>(z, sm2 + h * NP, tt, tw);
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < E; ++s) sm2[h * NP + swz<LOGE>(fft_out_index<N1, E>(tt, s))] = z[s];
+      __syncthreads();
+      const int i0 = 2 * p, i1 = 2 * p + 1;
+      const double ac0 = R.ac[i0], as0 = R.as[i0], bc0 = R.bc[i0], bs0 = R.bs[i0];
+      const double ac1 = R.ac[i1], as1 = R.as[i1], bc1 = R.bc[i1], bs1 = R.bs[i1];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        if (rp[q] == 0.0) continue;
+        const long long k = kq[q];
+        const int k2 = (int)(k % L2);
+        const long long k1 = k / L2;
+        const int hk = (k2 == k2a) ? 0 : 1;
+        const long long kp = 2 * L - k;
+        const int k2p = (int)(kp % L2);
+        const long long k1p = kp / L2;
+        const int hp = (k2p == k2a) ? 0 : 1;
+        const double2 Zk = sm2[hk * NP + swz<LOGE>((int)k1)];
+        const double2 Zp = cconj(sm2[hp * NP + swz<LOGE>((int)k1p)]);
+        double2 Ya = make_double2(0.5 * (Zk.x + Zp.x), 0.5 * (Zk.y + Zp.y));
+        double2 Yb = make_double2(0.5 * (Zk.y - Zp.y), -0.5 * (Zk.x - Zp.x));
+        if (k == L) { Ya.y = 0.0; Yb.y = 0.0; }      // S u has no row N (schlomilch.py:314-316)
+        const double2 th = cs[tid + NT * q];
+        const double A0 = ac0 * th.x + as0 * th.y, B0 = bc0 * th.x + bs0 * th.y;
+        const double A1 = ac1 * th.x + as1 * th.y, B1 = bc1 * th.x + bs1 * th.y;
+        const double r0 = rp[q], r1 = r0 * ir[q];
+        acc[q] += r0 * (A0 * Ya.x + B0 * Ya.y) + r1 * (A1 * Yb.x + B1 * Yb.y);
+        rp[q] = r1 * ir[q];
+      }
+    }
+    // flush when the next unit belongs to another vector
+    const bool last = (u + 1 == vr.y) || (a.units[u + 1].vec != U.vec);
+    if (last) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const long long k = kq[q];
+        if (k && ((k - a.first) % a.stride) == 0 && k >= a.first) {
+          const long long j = (k - a.first) / a.stride;
+          double* dst = a.F + (long long)U.vec * a.ldf + j;
+          *dst += acc[q];
+        }
+        acc[q] = 0.0;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- launch
+template <int N2>
+static cudaError_t p1_t(const FarArgs& a, int n_units, cudaStream_t st) {
+  constexpr int E = N2 >= 16 ? 16 : N2;
+  constexpr int W = N2 >= 4096 ? 1 : 4096 / N2;
+  constexpr int T = N2 / E;
+  constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
+  const int smem = W * (N2 + PAD) * 16;
+  auto k = far_pass1_kernel<N2, E, W>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k<<<dim3(a.L1 / W, n_units), W * T, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int N1, bool ONE>
+static cudaError_t p2_t(const FarArgs& a, int gx, int gy, cudaStream_t st) {
+  constexpr int E = N1 >= 16 ? 16 : N1;
+  constexpr int T = N1 / E;
+  constexpr int NCOL = ONE ? 1 : 2;
+  constexpr int NQ = E / 2 > 0 ? E / 2 : 1;
+  const int smem = (NCOL * (N1 + 4) + NCOL * T * NQ) * 16;
+  auto k = far_pass2_kernel<N1, E, ONE>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k<<<dim3(gx, gy), NCOL * T, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_far_pass1(const FarArgs& a, int logN2, int n_units, cudaStream_t st) {
+  switch (logN2) {
+    case 6: return p1_t<64>(a, n_units, st);
+    case 7: return p1_t<128>(a, n_units, st);
+    case 8: return p1_t<256>(a, n_units, st);
+    case 9: return p1_t<512>(a, n_units, st);
+    case 10: return p1_t<1024>(a, n_units, st);
+    case 11: return p1_t<2048>(a, n_units, st);
+    case 12: return p1_t<4096>(a, n_units, st);
+    case 13: return p1_t<8192>(a, n_units, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_far_pass2(const FarArgs& a, int logN1, cudaStream_t st) {
+  const int gx = a.L2 / 2 + 1;
+  switch (logN1) {
+    case 7: return p2_t<128, false>(a, gx, 1, st);
+    case 8: return p2_t<256, false>(a, gx, 1, st);
+    case 9: return p2_t<512, false>(a, gx, 1, st);
+    case 10: return p2_t<1024, false>(a, gx, 1, st);
+    case 11: return p2_t<2048, false>(a, gx, 1, st);
+    case 12: return p2_t<4096, false>(a, gx, 1, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_far_onepass(const FarArgs& a, int logN1, int n_ranges, cudaStream_t st) {
+  switch (logN1) {
+    case 1: return p2_t<2, true>(a, 1, n_ranges, st);
+    case 2: return p2_t<4, true>(a, 1, n_ranges, st);
+    case 3: return p2_t<8, true>(a, 1, n_ranges, st);
+    case 4: return p2_t<16, true>(a, 1, n_ranges, st);
+    case 5: return p2_t<32, true>(a, 1, n_ranges, st);
+    case 6: return p2_t<64, true>(a, 1, n_ranges, st);
+    case 7: return p2_t<128, true>(a, 1, n_ranges, st);
+    case 8: return p2_t<256, true>(a, 1, n_ranges, st);
+    case 9: return p2_t<512, true>(a, 1, n_ranges, st);
+    case 10: return p2_t<1024, true>(a, 1, n_ranges, st);
+    case 11: return p2_t<2048, true>(a, 1, n_ranges, st);
+    case 12: return p2_t<4096, true>(a, 1, n_ranges, st);
+    case 13: return p2_t<8192, true>(a, 1, n_ranges, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace fhtb

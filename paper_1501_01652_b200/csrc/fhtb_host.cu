@@ -1,0 +1,939 @@
+// fhtb_host.cu -- host runtime behind the C ABI (include/fhtb200.h).
+//
+// Owns the per-device tables (FFT twiddles, Bessel order constants), the
+// grid objects (partition + far/near-field tables on the device) and the
+// apply scheduler: request packing, far-field unit ordering and chunking,
+// near-field tiling and vector grouping.  All scheduling decisions are
+// deterministic functions of the arguments, so results are reproducible.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fhtb200.h"
+#include "fhtb_bessel.cuh"
+#include "fhtb_launch.h"
+
+using namespace fhtb;
+
+namespace {
+
+thread_local std::string g_err;
+int64_t g_far_chunk_bytes = 1LL << 30;     // two-pass intermediate budget
+int64_t g_near_chunk_cols = 8192;          // near-field column chunk per tile
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(x)                                                                       \
+  do {                                                                              \
+    cudaError_t e_ = (x);                                                           \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(FHTB_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+// ------------------------------------------------------------ host math
+// a_0..a_{count-1}(nu) by the ratio recurrence (bessel.py:45-58)
+std::vector<double> asy_coeffs(int nu, int count) {
+  std::vector<double> a(count);
+  a[0] = 1.0;
+  const double q = 4.0 * nu * nu;
+  for (int m = 1; m < count; ++m) {
+    const double t = (double)(2 * m - 1);
+    a[m] = a[m - 1] * (q - t * t) / (8.0 * m);
+  }
+  return a;
+}
+
+// s_{nu,M}(eps), four fixed-point iterations (bessel.py:109-130)
+double asy_cutoff(int nu, int mt, double eps) {
+  std::vector<double> a = asy_coeffs(nu, 2 * mt + 2);
+  const double a0 = std::fabs(a[2 * mt]), a1 = std::fabs(a[2 * mt + 1]);
+  const double c = std::sqrt(2.0) / (std::sqrt(M_PI) * eps);
+  double s = 1.0;
+  for (int i = 0; i < 4; ++i) s = std::pow(c * (a0 + a1 / s), 1.0 / (2 * mt + 0.5));
+  return s;
+}
+
+// t_{nu,T}(eps) (bessel.py:149-168)
+double taylor_cutoff(int nu, int nt, double eps) {
+  const double e = 2 * nt + nu;
+  const double lt = (e * std::log(2.0) + std::lgamma(nt + nu + 1.0) + std::lgamma(nt + 1.0) + std::log(eps)) / e;
+  return std::exp(lt);
+}
+
+JOrder make_jorder(int nu) {
+  JOrder c;
+  const double u = std::ldexp(1.0, -52);
+  c.tlo = taylor_cutoff(nu, kTaylorTerms, u);
+  c.shi = asy_cutoff(nu, kAsyPairs, u);
+  c.inv_fact = 1.0 / std::tgamma(nu + 1.0);
+  const double r = std::sqrt(0.5);
+  switch ((2 * nu + 1) % 8) {
+    case 1: c.cphi = r; c.sphi = r; break;
+    case 3: c.cphi = -r; c.sphi = r; break;
+    case 5: c.cphi = -r; c.sphi = -r; break;
+    default: c.cphi = r; c.sphi = -r; break;
+  }
+  std::vector<double> a = asy_coeffs(nu, 2 * kAsyPairs);
+  for (int m = 0; m < kAsyPairs; ++m) {
+    const double sg = (m & 1) ? -1.0 : 1.0;
+    c.ae[m] = sg * a[2 * m];
+    c.ao[m] = sg * a[2 * m + 1];
+  }
+  return c;
+}
+
+// ------------------------------------------------------- device context
+constexpr int kTwMaxLog = 13;
+
+struct DevCtx {
+  double2* tw = nullptr;           // twiddle pool, N = 2..8192
+  JOrder* jtab = nullptr;          // orders 0..kMaxOrder
+  unsigned long long* scratch = nullptr;
+  std::map<int, std::pair<double2*, double2*>> qtab;   // four-step twiddles per log2 Q
+};
+
+constexpr int kQBits = 12;
+inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+std::mutex g_mu;
+std::map<int, DevCtx> g_ctx;
+
+int get_ctx(DevCtx** out) {
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_ctx.find(dev);
+  if (it != g_ctx.end()) {
+    *out = &it->second;
+    return FHTB_OK;
+  }
+  DevCtx c;
+  const long long ntw = (1LL << (kTwMaxLog + 1)) - 2;
+  CU(cudaMalloc(&c.tw, ntw * sizeof(double2)));
+  CU(launch_twiddles(c.tw, kTwMaxLog, 0));
+  std::vector<JOrder> tab(kMaxOrder + 1);
+  for (int o = 0; o <= kMaxOrder; ++o) tab[o] = make_jorder(o);
+  CU(cudaMalloc(&c.jtab, tab.size() * sizeof(JOrder)));
+  CU(cudaMemcpy(c.jtab, tab.data(), tab.size() * sizeof(JOrder), cudaMemcpyHostToDevice));
+  CU(cudaMalloc(&c.scratch, 64));
+  CU(cudaDeviceSynchronize());
+  g_ctx[dev] = c;
+  *out = &g_ctx[dev];
+  return FHTB_OK;
+}
+
+// e^{+2 pi i m / Q} = qlo[m & (2^b - 1)] * qhi[m >> b],  b = min(12, log2 Q)
+int get_qtab(DevCtx* c, int logQ, double2** lo, double2** hi, int* bits) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  const int b = std::min(kQBits, logQ);
+  auto it = c->qtab.find(logQ);
+  if (it == c->qtab.end()) {
+    double2 *ql = nullptr, *qh = nullptr;
+    const long long nlo = 1LL << b, nhi = (1LL << logQ) >> b;
+    CU(cudaMalloc(&ql, nlo * sizeof(double2)));
+    CU(cudaMalloc(&qh, nhi * sizeof(double2)));
+    CU(launch_qtwiddles(ql, qh, logQ, b, 1, 0));
+    CU(cudaDeviceSynchronize());
+    it = c->qtab.emplace(logQ, std::make_pair(ql, qh)).first;
+  }
+  *lo = it->second.first;
+  *hi = it->second.second;
+  *bits = b;
+  return FHTB_OK;
+}
+
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Bump allocator over a caller-provided workspace.
+struct Carve {
+  char* base;
+  size_t cap, off = 0;
+  bool ok = true;
+  template <class T> T* take(size_t n) {
+    size_t b = align_up(n * sizeof(T));
+    if (off + b > cap) { ok = false; return nullptr; }
+    T* p = (T*)(base + off);
+    off += b;
+    return p;
+  }
+};
+
+bool is_pow2(long long x) { return x > 0 && (x & (x - 1)) == 0; }
+int ilog2ll(long long x) { int l = 0; while ((1LL << l) < x) ++l; return l; }
+
+// Request packing (schlomilch.py:280-299 with the order combination folded
+// into per-term scalars; see fhtb_types.h).
+int pack_requests(const fhtb_request* reqs, int n_req, int M, const std::vector<int>& universe,
+                  long long n_data_cols, std::vector<ReqDesc>& out) {
+  out.assign(n_req, ReqDesc());
+  const double sq2pi = std::sqrt(2.0 / M_PI);
+  for (int q = 0; q < n_req; ++q) {
+    const fhtb_request& r = reqs[q];
+    ReqDesc d;
+    std::memset(&d, 0, sizeof(d));
+    d.vec = r.vec;
+    d.pa = r.pre_a_pow;
+    d.pb = r.pre_b_pow;
+    d.pr = r.post_r_pow;
+    d.pe = r.post_e_pow;
+    d.col_lo = std::max<long long>(r.col_lo, 1);
+    d.preA = r.pre_a_pow ? r.pre_a : nullptr;
+    d.preB = r.pre_b_pow ? r.pre_b : nullptr;
+    d.post_e = r.post_e_pow ? r.post_e : nullptr;
+    if (r.n_terms < 0 || (r.n_terms && (!r.orders || !r.weights)))
+      return fail(FHTB_EINVAL, "request order list is malformed");
+    for (int t = 0; t < r.n_terms; ++t) {
+      const int o = r.orders[t];
+      const double w = r.weights[t];
+      if (o < 0 || o > kMaxOrder) return fail(FHTB_EINVAL, "order out of range");
+      auto it = std::find(universe.begin(), universe.end(), o);
+      if (it == universe.end()) return fail(FHTB_EINVAL, "order " + std::to_string(o) + " outside engine universe");
+      d.w[it - universe.begin()] += w;
+      // far field scalars
+      std::vector<double> a = asy_coeffs(o, 2 * M);
+      const double rr = std::sqrt(0.5);
+      double cp, sp;
+      switch ((2 * o + 1) % 8) {
+        case 1: cp = rr; sp = rr; break;
+        case 3: cp = -rr; sp = rr; break;
+        case 5: cp = -rr; sp = -rr; break;
+        default: cp = rr; sp = -rr; break;
+      }
+      for (int m = 0; m < M; ++m) {
+        const double lam = w * sq2pi * ((m & 1) ? -1.0 : 1.0);
+        const double g = lam * a[2 * m], h = lam * a[2 * m + 1];
+        d.ac[2 * m] += g * cp;  d.as[2 * m] += -g * sp;
+        d.bc[2 * m] += g * sp;  d.bs[2 * m] += g * cp;
+        d.ac[2 * m + 1] += h * sp;  d.as[2 * m + 1] += h * cp;
+        d.bc[2 * m + 1] += -h * cp; d.bs[2 * m + 1] += h * sp;
+      }
+    }
+    (void)n_data_cols;
+    out[q] = d;
+  }
+  return FHTB_OK;
+}
+
+// Group request columns (sorted by vector) so each group holds whole vectors
+// and at most 64 request columns.
+int make_groups(const std::vector<ReqDesc>& sorted, int n_vec, std::vector<int>& q0, std::vector<int>& v0) {
+  q0.clear();
+  v0.clear();
+  std::vector<int> cnt(n_vec, 0);
+  for (auto& r : sorted) cnt[r.vec]++;
+  int q = 0, v = 0;
+  while (v < n_vec) {
+    q0.push_back(q);
+    v0.push_back(v);
+    int cols = 0;
+    while (v < n_vec && cols + cnt[v] <= 64) { cols += cnt[v]; q += cnt[v]; ++v; }
+    if (cols == 0) return fail(FHTB_EINVAL, "more than 64 requests for one vector");
+  }
+  q0.push_back(q);
+  v0.push_back(v);
+  return FHTB_OK;
+}
+
+// Near tiles over a list of segments (r0, r1, c_end) in grid index space.
+void make_tiles(const std::vector<long long>& segs, long long first, long long stride, long long n_data_cols,
+                long long n_out, std::vector<NearTile>& tiles, std::vector<NearRowTile>& rts, long long& n_slots) {
+  tiles.clear();
+  rts.clear();
+  n_slots = 0;
+  const int ns = (int)segs.size() / 3;
+  for (int s = 0; s < ns; ++s) {
+    const long long r0 = segs[3 * s], r1 = segs[3 * s + 1], ce = segs[3 * s + 2];
+    const long long cb = std::min(ce, n_data_cols + 1);
+    if (r1 <= r0 || cb <= 1) continue;
+    // output rows j with grid row k = first + stride*j in [r0, r1)
+    long long jlo = (r0 - first + stride - 1) / stride;
+    if (r0 < first) jlo = 0;
+    long long jhi = (r1 - 1 - first) >= 0 ? (r1 - 1 - first) / stride + 1 : 0;
+    jhi = std::min(jhi, n_out);     // grid rows past the last output row are not outputs
+    if (jhi <= jlo) continue;
+    const long long nch = (cb - 1 + g_near_chunk_cols - 1) / g_near_chunk_cols;
+    for (long long j = jlo; j < jhi; j += kNearRT) {
+      const int nr = (int)std::min<long long>(kNearRT, jhi - j);
+      long long slot = -1;
+      if (nch > 1) {
+        slot = n_slots;
+        n_slots += nch;
+        rts.push_back(NearRowTile{j, nr, (int)nch, slot});
+      }
+      for (long long c = 0; c < nch; ++c) {
+        NearTile t;
+        t.seg = s;
+        t.nrows = nr;
+        t.j0 = j;
+        t.na = 1 + c * g_near_chunk_cols;
+        t.nb = std::min(cb, t.na + g_near_chunk_cols);
+        t.part = nch > 1 ? slot + c : -1;
+        tiles.push_back(t);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+// ======================================================================
+// ======================================================================
+struct fhtb_grid {
+  int device = 0;
+  long long L = 0;
+  double gamma = 0;
+  int M = 0;
+  long long first = 1, stride = 1, n_out = 0, n_data_cols = 0;
+  std::vector<long long> blocks;   // 4 per block
+  std::vector<long long> segs;     // 3 per segment
+  std::vector<int> orders;
+  bool direct = false;             // direct (power-of-two) far-field mode
+  int logQ = 0, logN1 = 0, logN2 = 0;   // direct mode split
+  std::vector<BlockDesc> bdesc;    // host copy (chirp parameters)
+  std::vector<double2*> H;         // chirp filter spectra per block
+  BlockDesc* d_blocks = nullptr;
+  // near field
+  std::vector<NearTile> tiles;
+  std::vector<NearRowTile> rts;
+  long long n_slots = 0;
+  NearTile* d_tiles = nullptr;
+  NearRowTile* d_rts = nullptr;
+};
+
+namespace {
+
+void split_q(int logQ, int* l1, int* l2) {
+  *l1 = (logQ + 1) / 2;
+  *l2 = logQ - *l1;
+}
+
+// Forward FFT (sign -1) of a length-2^logQ device vector (filter spectra).
+int plain_fft(DevCtx* ctx, int logQ, const double2* in, double2* tmp, double2* out, cudaStream_t st) {
+  if (logQ <= 11) {
+    CU(launch_fft_batch(logQ, -1, in, out, 1, ctx->tw, st));
+    return FHTB_OK;
+  }
+  FarArgs a;
+  std::memset(&a, 0, sizeof a);
+  int l1, l2;
+  split_q(logQ, &l1, &l2);
+  a.L1 = 1 << l1;
+  a.L2 = 1 << l2;
+  a.tw = ctx->tw;
+  double2 *ql, *qh;
+  int qb;
+  if (int r = get_qtab(ctx, logQ, &ql, &qh, &qb)) return r;
+  a.qlo = ql;
+  a.qhi = qh;
+  a.qbits = qb;
+  CU(launch_plain_fft(a, l1, l2, in, tmp, out, st));
+  return FHTB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fhtb_abi_version(void) { return 1; }
+const char* fhtb_last_error(void) { return g_err.c_str(); }
+
+int fhtb_init(void) {
+  DevCtx* c;
+  return get_ctx(&c);
+}
+
+int fhtb_set_option(const char* key, int64_t value) {
+  if (!key) return fail(FHTB_EINVAL, "null key");
+  if (!std::strcmp(key, "far_chunk_bytes")) {
+    if (value < (1 << 20)) return fail(FHTB_EINVAL, "far_chunk_bytes too small");
+    g_far_chunk_bytes = value;
+    return FHTB_OK;
+  }
+  if (!std::strcmp(key, "near_chunk_cols")) {
+    if (value < 64) return fail(FHTB_EINVAL, "near_chunk_cols too small");
+    g_near_chunk_cols = value;
+    return FHTB_OK;
+  }
+  return fail(FHTB_EINVAL, std::string("unknown option ") + key);
+}
+
+// ------------------------------------------------------------------- L1
+int fhtb_bessel_j(int nu, const double* z, int64_t n, double* out, void* stream) {
+  if (nu < 0) return fail(FHTB_EINVAL, "bessel_j requires nu >= 0");
+  DevCtx* c;
+  if (int r = get_ctx(&c)) return r;
+  JOrder jo = make_jorder(nu);
+  CU(launch_bessel_j(nu, jo, z, n, out, S(stream)));
+  return FHTB_OK;
+}
+
+int fhtb_bessel_j_multi(int nu_max, const double* z, int64_t n, double* out, void* stream) {
+  if (nu_max < 0 || nu_max >= kMaxOrd) return fail(FHTB_EINVAL, "nu_max out of range");
+  DevCtx* c;
+  if (int r = get_ctx(&c)) return r;
+  CU(launch_bessel_multi(nu_max, c->jtab, z, n, out, S(stream)));
+  return FHTB_OK;
+}
+
+int fhtb_hankel_asy_eval(int nu, int m_terms, const double* z, int64_t n, double* out, void* stream) {
+  if (nu < 0 || m_terms < 1 || m_terms > 64) return fail(FHTB_EINVAL, "bad hankel_asy_eval arguments");
+  DevCtx* c;
+  if (int r = get_ctx(&c)) return r;
+  std::vector<double> a = asy_coeffs(nu, 2 * m_terms), coef(2 * m_terms);
+  for (int m = 0; m < m_terms; ++m) {
+    const double sg = (m & 1) ? -1.0 : 1.0;
+    coef[m] = sg * a[2 * m];
+    coef[m_terms + m] = sg * a[2 * m + 1];
+  }
+  double* d = nullptr;
+  CU(cudaMallocAsync(&d, coef.size() * sizeof(double), S(stream)));
+  CU(cudaMemcpyAsync(d, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice, S(stream)));
+  CU(launch_hankel_eval(nu, m_terms, d, z, n, out, S(stream)));
+  CU(cudaFreeAsync(d, S(stream)));
+  CU(cudaStreamSynchronize(S(stream)));
+  return FHTB_OK;
+}
+
+int fhtb_taylor_eval(int nu, int n_terms, const double* z, int64_t n, double* out, void* stream) {
+  if (nu < 0 || n_terms < 1) return fail(FHTB_EINVAL, "bad taylor_eval arguments");
+  DevCtx* c;
+  if (int r = get_ctx(&c)) return r;
+  CU(launch_taylor_eval(nu, n_terms, 1.0 / std::tgamma(nu + 1.0), z, n, out, S(stream)));
+  return FHTB_OK;
+}
+
+int fhtb_roots_j0(int64_t count, double* roots, double* perturb, double* resid_max, void* stream) {
+  if (count < 1) return fail(FHTB_EINVAL, "count must be >= 1");
+  DevCtx* c;
+  if (int r = get_ctx(&c)) return r;
+  CU(cudaMemsetAsync(c->scratch, 0, 8, S(stream)));
+  CU(launch_roots_j0(c->jtab, count, roots, perturb, c->scratch, S(stream)));
+  unsigned long long bits = 0;
+  CU(cudaMemcpyAsync(&bits, c->scratch, 8, cudaMemcpyDeviceToHost, S(stream)));
+  CU(cudaStreamSynchronize(S(stream)));
+  double res;
+  std::memcpy(&res, &bits, 8);
+  if (resid_max) *resid_max = res;
+  if (!(res <= 1e-13)) {
+    char buf[128];
+    std::snprintf(buf, sizeof buf, "Newton failed to converge on J0 roots (residual %.3e)", res);
+    return fail(FHTB_ECONVERGE, buf);
+  }
+  return FHTB_OK;
+}
+
+int fhtb_fft(int64_t n, int sign, const double* in, double* out, int64_t batch, void* stream) {
+  if (!is_pow2(n) || n < 2 || n > 2048) return fail(FHTB_EINVAL, "fhtb_fft: n must be a power of two in [2, 2048]");
+  DevCtx* c;
+  if (int r = get_ctx(&c)) return r;
+  CU(launch_fft_batch(ilog2ll(n), sign, (const double2*)in, (double2*)out, batch, c->tw, S(stream)));
+  return FHTB_OK;
+}
+
+// ---------------------------------------------------------------- grid
+int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
+  if (!d || !out) return fail(FHTB_EINVAL, "null argument");
+  if (d->L < 1) return fail(FHTB_EINVAL, "L must be >= 1");
+  if (d->m_terms < 1 || 2 * d->m_terms > kMaxTerms) return fail(FHTB_EINVAL, "m_terms out of range");
+  if (d->n_orders < 1 || d->n_orders > kMaxOrd) return fail(FHTB_EINVAL, "order universe size out of range");
+  if (d->row_stride < 1 || d->row_first < 1) return fail(FHTB_EINVAL, "bad row mapping");
+  DevCtx* ctx;
+  if (int r = get_ctx(&ctx)) return r;
+  fhtb_grid* g = new fhtb_grid();
+  CU(cudaGetDevice(&g->device));
+  g->L = d->L;
+  g->gamma = d->gamma;
+  g->M = d->m_terms;
+  g->first = d->row_first;
+  g->stride = d->row_stride;
+  g->n_out = d->n_out;
+  g->n_data_cols = std::min<long long>(d->n_data_cols, d->L);
+  g->blocks.assign(d->blocks, d->blocks + 4 * d->n_blocks);
+  g->segs.assign(d->segments, d->segments + 3 * d->n_segments);
+  g->orders.assign(d->orders, d->orders + d->n_orders);
+  for (int o : g->orders)
+    if (o < 0 || o > kMaxOrder) { delete g; return fail(FHTB_EINVAL, "order out of range"); }
+  g->direct = is_pow2(2 * g->L) && g->first == 1 && g->stride == 1 && g->n_out == g->L;
+  if (g->direct) {
+    g->logQ = ilog2ll(2 * g->L);
+    if (g->logQ > 25) { delete g; return fail(FHTB_EINVAL, "grid too large (2L > 2^25)"); }
+    if (g->logQ <= 13) {
+      g->logN1 = g->logQ;
+      g->logN2 = 0;
+    } else {
+      g->logN1 = std::min(12, (g->logQ + 1) / 2);
+      g->logN2 = g->logQ - g->logN1;
+    }
+  }
+  const int nb = d->n_blocks;
+  g->H.assign(nb, nullptr);
+  for (int b = 0; b < nb; ++b) {
+    BlockDesc x;
+    std::memset(&x, 0, sizeof x);
+    x.r0 = g->blocks[4 * b];
+    x.r1 = g->blocks[4 * b + 1];
+    x.c0 = g->blocks[4 * b + 2];
+    x.c1 = g->blocks[4 * b + 3];
+    if (!g->direct) {
+      // rows j with first + stride*j < r1 ; columns c0 .. min(c1, data+1)
+      const long long J = std::min<long long>(g->n_out, x.r1 > g->first ? (x.r1 - g->first + g->stride - 1) / g->stride : 0);
+      const long long Mn = std::min(x.c1, g->n_data_cols + 1) - x.c0;
+      if (J > 0 && Mn > 0 && x.r1 > x.r0) {
+        const int logQ = std::max(2, ilog2ll(Mn + J - 1));
+        if (logQ > 26) { fhtb_grid_destroy(g); return fail(FHTB_EINVAL, "chirp convolution too long"); }
+        const long long Q = 1LL << logQ;
+        x.J = J;
+        x.Mn = Mn;
+        x.logQ = logQ;
+        double2 *h = nullptr, *tmp = nullptr, *Hb = nullptr;
+        CU(cudaMalloc(&h, Q * sizeof(double2)));
+        CU(cudaMalloc(&tmp, Q * sizeof(double2)));
+        CU(cudaMalloc(&Hb, Q * sizeof(double2)));
+        CU(launch_chirp_filter(h, Q, Mn, J, g->stride, g->L, 0));
+        if (int r = plain_fft(ctx, logQ, h, tmp, Hb, 0)) return r;
+        CU(cudaDeviceSynchronize());
+        cudaFree(h);
+        cudaFree(tmp);
+        x.H = Hb;
+        g->H[b] = Hb;
+      } else {
+        x.J = 0;
+        x.Mn = 0;
+      }
+    }
+    g->bdesc.push_back(x);
+  }
+  if (!g->bdesc.empty()) {
+    CU(cudaMalloc(&g->d_blocks, g->bdesc.size() * sizeof(BlockDesc)));
+    CU(cudaMemcpy(g->d_blocks, g->bdesc.data(), g->bdesc.size() * sizeof(BlockDesc), cudaMemcpyHostToDevice));
+  }
+  if (g->direct && g->logN2 > 0) {
+    double2 *ql, *qh;
+    int qb;
+    if (int r = get_qtab(ctx, g->logQ, &ql, &qh, &qb)) return r;
+  }
+  make_tiles(g->segs, g->first, g->stride, g->n_data_cols, g->n_out, g->tiles, g->rts, g->n_slots);
+  if (!g->tiles.empty()) {
+    CU(cudaMalloc(&g->d_tiles, g->tiles.size() * sizeof(NearTile)));
+    CU(cudaMemcpy(g->d_tiles, g->tiles.data(), g->tiles.size() * sizeof(NearTile), cudaMemcpyHostToDevice));
+  }
+  if (!g->rts.empty()) {
+    CU(cudaMalloc(&g->d_rts, g->rts.size() * sizeof(NearRowTile)));
+    CU(cudaMemcpy(g->d_rts, g->rts.data(), g->rts.size() * sizeof(NearRowTile), cudaMemcpyHostToDevice));
+  }
+  CU(cudaDeviceSynchronize());
+  *out = g;
+  return FHTB_OK;
+}
+
+void fhtb_grid_destroy(fhtb_grid* g) {
+  if (!g) return;
+  cudaFree(g->d_blocks);
+  for (double2* h : g->H) cudaFree(h);
+  cudaFree(g->d_tiles);
+  cudaFree(g->d_rts);
+  delete g;
+}
+
+}  // extern "C"
+
+namespace {
+
+// bytes of intermediate per far-field unit
+size_t unit_bytes_q(const fhtb_grid* g, int logQ) {
+  return (size_t)(g->direct ? g->M : 2 * g->M) * ((size_t)1 << logQ) * sizeof(double2);
+}
+
+long long chunk_for(size_t ub, long long n_units) {
+  long long per = std::max<long long>(1, g_far_chunk_bytes / (long long)ub);
+  return std::min(per, std::max<long long>(n_units, 1));
+}
+
+struct FarPlan {
+  std::vector<UnitDesc> units;                 // execution order
+  std::vector<int2> chunks;                    // [u0, u1) per launch group
+  std::vector<int> chunk_logq;
+  size_t g_bytes = 0;                          // intermediate
+  size_t part_bytes = 0;                       // chirp partials
+};
+
+void plan_far(const fhtb_grid* g, const std::vector<ReqDesc>& rs, FarPlan& fp) {
+  fp = FarPlan();
+  const int nb = (int)g->blocks.size() / 4;
+  const int n_req = (int)rs.size();
+  std::vector<UnitDesc> all;
+  for (int q = 0; q < n_req; ++q)
+    for (int b = 0; b < nb; ++b) {
+      const long long r0 = g->blocks[4 * b], r1 = g->blocks[4 * b + 1];
+      const long long c0 = std::max<long long>(g->blocks[4 * b + 2], rs[q].col_lo);
+      const long long c1 = std::min<long long>(g->blocks[4 * b + 3], g->n_data_cols + 1);
+      if (r1 <= r0 || c1 <= c0) continue;
+      if (!g->direct && g->bdesc[b].J == 0) continue;
+      all.push_back(UnitDesc{q, b, rs[q].vec, 0});
+    }
+  if (g->direct) {
+    fp.units = all;
+    const long long nu = (long long)all.size();
+    if (g->logN2 == 0) {
+      long long u = 0;
+      while (u < nu) {
+        long long e = u;
+        while (e < nu && all[e].vec == all[u].vec) ++e;
+        fp.chunks.push_back(make_int2((int)u, (int)e));
+        fp.chunk_logq.push_back(g->logQ);
+        u = e;
+      }
+    } else {
+      const size_t ub = unit_bytes_q(g, g->logQ);
+      const long long cu = chunk_for(ub, nu);
+      for (long long u0 = 0; u0 < nu; u0 += cu) {
+        fp.chunks.push_back(make_int2((int)u0, (int)std::min(nu, u0 + cu)));
+        fp.chunk_logq.push_back(g->logQ);
+      }
+      if (nu) fp.g_bytes = ub * cu;
+    }
+    return;
+  }
+  // chirp mode: group by filter length, keep vector order inside a group
+  std::vector<int> logs;
+  for (auto& u : all) logs.push_back(g->bdesc[u.block].logQ);
+  std::sort(logs.begin(), logs.end());
+  logs.erase(std::unique(logs.begin(), logs.end()), logs.end());
+  for (int lq : logs) {
+    const long long start = (long long)fp.units.size();
+    for (auto& u : all)
+      if (g->bdesc[u.block].logQ == lq) fp.units.push_back(u);
+    const long long n = (long long)fp.units.size() - start;
+    const size_t ub = unit_bytes_q(g, lq);
+    const long long cu = chunk_for(ub, n);
+    for (long long u0 = 0; u0 < n; u0 += cu) {
+      fp.chunks.push_back(make_int2((int)(start + u0), (int)(start + std::min(n, u0 + cu))));
+      fp.chunk_logq.push_back(lq);
+    }
+    fp.g_bytes = std::max(fp.g_bytes, ub * (size_t)cu);
+    fp.part_bytes = std::max(fp.part_bytes, sizeof(double) * (size_t)cu * (size_t)g->n_out);
+  }
+}
+
+size_t far_ws(const fhtb_grid* g, int n_req) {
+  // worst case over request sets of this size: every request touches every block
+  std::vector<ReqDesc> rs(n_req);
+  for (int q = 0; q < n_req; ++q) { std::memset(&rs[q], 0, sizeof(ReqDesc)); rs[q].col_lo = 1; }
+  FarPlan fp;
+  plan_far(g, rs, fp);
+  size_t s = align_up(sizeof(UnitDesc) * std::max<size_t>(fp.units.size(), 1));
+  s += align_up(sizeof(int2) * (fp.chunks.size() + 1));
+  s += align_up(fp.g_bytes) + align_up(fp.part_bytes);
+  return s;
+}
+
+size_t ws_need(const fhtb_grid* g, int n_req, int n_vec, int flags) {
+  size_t s = align_up(sizeof(ReqDesc) * std::max(n_req, 1));
+  if (flags & FHTB_FAR) s += far_ws(g, n_req);
+  s += 2 * align_up(sizeof(int) * (n_vec + 2));
+  if (flags & FHTB_NEAR) s += align_up(sizeof(double) * (size_t)g->n_slots * n_vec * kNearRT);
+  return s + 4096;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t fhtb_apply_workspace(const fhtb_grid* g, int32_t n_req, int32_t n_vec, int32_t flags) {
+  if (!g) return 0;
+  return ws_need(g, n_req, n_vec, flags);
+}
+
+int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C, int64_t ldc,
+               int32_t n_vec, double* F, int64_t ldf, int32_t flags, void* ws, size_t ws_bytes, void* stream) {
+  if (!g) return fail(FHTB_EINVAL, "null grid");
+  if (n_req < 0 || n_vec < 0) return fail(FHTB_EINVAL, "negative counts");
+  if (n_req == 0 || n_vec == 0) return FHTB_OK;
+  for (int q = 0; q < n_req; ++q)
+    if (reqs[q].vec < 0 || reqs[q].vec >= n_vec) return fail(FHTB_EINVAL, "request vec out of range");
+  if (ws_bytes < ws_need(g, n_req, n_vec, flags)) return fail(FHTB_EINVAL, "workspace too small");
+  DevCtx* ctx;
+  if (int r = get_ctx(&ctx)) return r;
+  cudaStream_t st = S(stream);
+
+  std::vector<ReqDesc> rd;
+  if (int r = pack_requests(reqs, n_req, g->M, g->orders, g->n_data_cols, rd)) return r;
+  std::vector<int> perm(n_req);
+  for (int i = 0; i < n_req; ++i) perm[i] = i;
+  std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return rd[a].vec < rd[b].vec; });
+  std::vector<ReqDesc> rs(n_req);
+  for (int i = 0; i < n_req; ++i) rs[i] = rd[perm[i]];
+
+  Carve cv{(char*)ws, ws_bytes};
+  ReqDesc* d_req = cv.take<ReqDesc>(n_req);
+  CU(cudaMemcpyAsync(d_req, rs.data(), n_req * sizeof(ReqDesc), cudaMemcpyHostToDevice, st));
+
+  if ((flags & FHTB_FAR) && !g->blocks.empty()) {
+    FarPlan fp;
+    plan_far(g, rs, fp);
+    const long long nu = (long long)fp.units.size();
+    if (nu > 0) {
+      UnitDesc* d_units = cv.take<UnitDesc>(nu);
+      int2* d_ch = cv.take<int2>(fp.chunks.size());
+      double2* G = fp.g_bytes ? (double2*)cv.take<char>(fp.g_bytes) : nullptr;
+      double* part = fp.part_bytes ? (double*)cv.take<char>(fp.part_bytes) : nullptr;
+      if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small");
+      CU(cudaMemcpyAsync(d_units, fp.units.data(), nu * sizeof(UnitDesc), cudaMemcpyHostToDevice, st));
+      CU(cudaMemcpyAsync(d_ch, fp.chunks.data(), fp.chunks.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+      FarArgs a;
+      std::memset(&a, 0, sizeof a);
+      a.L = g->L;
+      a.M = g->M;
+      a.gamma = g->gamma;
+      a.Ld = (double)g->L;
+      a.pi_over_L = M_PI / (double)g->L;
+      a.first = g->first;
+      a.stride = g->stride;
+      a.n_out = g->n_out;
+      a.n_data_cols = g->n_data_cols;
+      a.units = d_units;
+      a.reqs = d_req;
+      a.blocks = g->d_blocks;
+      a.C = C;
+      a.ldc = ldc;
+      a.F = F;
+      a.ldf = ldf;
+      a.tw = ctx->tw;
+      a.G = G;
+      a.part = part;
+      a.part_stride = g->n_out;
+      if (g->direct && g->logN2 == 0) {
+        a.L1 = 1 << g->logN1;
+        a.L2 = 1;
+        a.logQ = g->logQ;
+        a.vranges = d_ch;
+        CU(launch_far_onepass(a, g->logN1, (int)fp.chunks.size(), st));
+      } else {
+        for (size_t ci = 0; ci < fp.chunks.size(); ++ci) {
+          const int lq = fp.chunk_logq[ci];
+          const int n_units = fp.chunks[ci].y - fp.chunks[ci].x;
+          double2 *ql, *qh;
+          int qb;
+          if (int r = get_qtab(ctx, lq, &ql, &qh, &qb)) return r;
+          a.qlo = ql;
+          a.qhi = qh;
+          a.qbits = qb;
+          a.logQ = lq;
+          a.u0 = fp.chunks[ci].x;
+          if (g->direct) {
+            a.L1 = 1 << g->logN1;
+            a.L2 = 1 << g->logN2;
+            a.vranges = d_ch + ci;
+            CU(launch_far_pass1(a, g->logN2, n_units, st));
+            CU(launch_far_pass2(a, g->logN1, st));
+          } else {
+            int l1, l2;
+            split_q(lq, &l1, &l2);
+            a.L1 = 1 << l1;
+            a.L2 = 1 << l2;
+            CU(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)n_units * g->n_out, st));
+            CU(launch_chirp_pass1(a, l2, n_units, st));
+            CU(launch_chirp_pass2(a, l1, n_units, st));
+            CU(launch_chirp_pass3(a, l2, n_units, st));
+            CU(launch_chirp_reduce(a, n_units, st));
+          }
+        }
+      }
+    }
+  }
+
+  if ((flags & FHTB_NEAR) && !g->tiles.empty()) {
+    std::vector<int> q0, v0;
+    if (int r = make_groups(rs, n_vec, q0, v0)) return r;
+    int* d_q0 = cv.take<int>(q0.size());
+    int* d_v0 = cv.take<int>(v0.size());
+    double* part = g->n_slots ? cv.take<double>((size_t)g->n_slots * n_vec * kNearRT) : nullptr;
+    if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small");
+    CU(cudaMemcpyAsync(d_q0, q0.data(), q0.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(d_v0, v0.data(), v0.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    NearArgs na;
+    std::memset(&na, 0, sizeof na);
+    na.tiles = g->d_tiles;
+    na.first = g->first;
+    na.stride = g->stride;
+    na.rowv = nullptr;
+    na.colv = nullptr;
+    na.gamma = g->gamma;
+    na.scale = M_PI / (double)g->L;
+    na.Ld = (double)g->L;
+    na.n_orders = (int)g->orders.size();
+    na.omax = 0;
+    for (int i = 0; i < na.n_orders; ++i) {
+      na.orders[i] = g->orders[i];
+      na.omax = std::max(na.omax, g->orders[i]);
+    }
+    na.jtab = ctx->jtab;
+    na.reqs = d_req;
+    na.grp_q0 = d_q0;
+    na.grp_v0 = d_v0;
+    na.C = C;
+    na.ldc = ldc;
+    na.n_data_cols = g->n_data_cols;
+    na.F = F;
+    na.ldf = ldf;
+    na.part = part;
+    na.part_stride = (long long)n_vec * kNearRT;
+    na.overwrite = 0;
+    CU(launch_near(na, (int)g->tiles.size(), (int)q0.size() - 1, st));
+    CU(launch_near_reduce(g->d_rts, (int)g->rts.size(), part, F, ldf, n_vec, 0, st));
+  }
+  return FHTB_OK;
+}
+
+// --------------------------------------------------------------- direct
+namespace {
+void direct_tiles(const fhtb_direct_desc* d, std::vector<NearTile>& tiles, std::vector<NearRowTile>& rts,
+                  long long& n_slots) {
+  std::vector<long long> seg = {1, d->n_rows + 1, d->n_cols + 1};
+  make_tiles(seg, 1, 1, std::min(d->n_data_cols, d->n_cols), d->n_rows, tiles, rts, n_slots);
+}
+}  // namespace
+
+size_t fhtb_direct_workspace(const fhtb_direct_desc* d, int32_t n_req, int32_t n_vec) {
+  if (!d) return 0;
+  std::vector<NearTile> tiles;
+  std::vector<NearRowTile> rts;
+  long long ns = 0;
+  direct_tiles(d, tiles, rts, ns);
+  size_t s = align_up(sizeof(ReqDesc) * std::max(n_req, 1));
+  s += align_up(sizeof(NearTile) * std::max<size_t>(tiles.size(), 1));
+  s += align_up(sizeof(NearRowTile) * std::max<size_t>(rts.size(), 1));
+  s += 2 * align_up(sizeof(int) * (n_vec + 2));
+  s += align_up(sizeof(double) * (size_t)ns * n_vec * kNearRT);
+  return s + 4096;
+}
+
+int fhtb_direct_apply(const fhtb_direct_desc* d, const fhtb_request* reqs, int32_t n_req, const double* C,
+                      int64_t ldc, int32_t n_vec, double* F, int64_t ldf, int32_t flags, void* ws,
+                      size_t ws_bytes, void* stream) {
+  if (!d) return fail(FHTB_EINVAL, "null descriptor");
+  if (d->n_orders < 1 || d->n_orders > kMaxOrd) return fail(FHTB_EINVAL, "order universe size out of range");
+  if (n_req == 0 || n_vec == 0 || d->n_rows == 0) return FHTB_OK;
+  for (int q = 0; q < n_req; ++q)
+    if (reqs[q].vec < 0 || reqs[q].vec >= n_vec) return fail(FHTB_EINVAL, "request vec out of range");
+  if (ws_bytes < fhtb_direct_workspace(d, n_req, n_vec)) return fail(FHTB_EINVAL, "workspace too small");
+  DevCtx* ctx;
+  if (int r = get_ctx(&ctx)) return r;
+  cudaStream_t st = S(stream);
+  std::vector<int> uni(d->orders, d->orders + d->n_orders);
+  std::vector<ReqDesc> rd;
+  if (int r = pack_requests(reqs, n_req, 1, uni, d->n_data_cols, rd)) return r;
+  std::vector<int> perm(n_req);
+  for (int i = 0; i < n_req; ++i) perm[i] = i;
+  std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return rd[a].vec < rd[b].vec; });
+  std::vector<ReqDesc> rs(n_req);
+  for (int i = 0; i < n_req; ++i) rs[i] = rd[perm[i]];
+  std::vector<NearTile> tiles;
+  std::vector<NearRowTile> rts;
+  long long ns = 0;
+  direct_tiles(d, tiles, rts, ns);
+  std::vector<int> q0, v0;
+  if (int r = make_groups(rs, n_vec, q0, v0)) return r;
+  Carve cv{(char*)ws, ws_bytes};
+  ReqDesc* d_req = cv.take<ReqDesc>(n_req);
+  NearTile* d_tiles = cv.take<NearTile>(std::max<size_t>(tiles.size(), 1));
+  NearRowTile* d_rts = cv.take<NearRowTile>(std::max<size_t>(rts.size(), 1));
+  int* d_q0 = cv.take<int>(q0.size());
+  int* d_v0 = cv.take<int>(v0.size());
+  double* part = ns ? cv.take<double>((size_t)ns * n_vec * kNearRT) : nullptr;
+  if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small");
+  CU(cudaMemcpyAsync(d_req, rs.data(), n_req * sizeof(ReqDesc), cudaMemcpyHostToDevice, st));
+  if (!tiles.empty()) CU(cudaMemcpyAsync(d_tiles, tiles.data(), tiles.size() * sizeof(NearTile), cudaMemcpyHostToDevice, st));
+  if (!rts.empty()) CU(cudaMemcpyAsync(d_rts, rts.data(), rts.size() * sizeof(NearRowTile), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_q0, q0.data(), q0.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_v0, v0.data(), v0.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  NearArgs na;
+  std::memset(&na, 0, sizeof na);
+  na.tiles = d_tiles;
+  na.first = 1;
+  na.stride = 1;
+  na.rowv = d->row_val;
+  na.colv = d->col_val;
+  na.Ld = d->r_scale;
+  na.n_orders = d->n_orders;
+  for (int i = 0; i < d->n_orders; ++i) {
+    na.orders[i] = d->orders[i];
+    na.omax = std::max(na.omax, d->orders[i]);
+  }
+  na.jtab = ctx->jtab;
+  na.reqs = d_req;
+  na.grp_q0 = d_q0;
+  na.grp_v0 = d_v0;
+  na.C = C;
+  na.ldc = ldc;
+  na.n_data_cols = std::min(d->n_data_cols, d->n_cols);
+  na.F = F;
+  na.ldf = ldf;
+  na.part = part;
+  na.part_stride = (long long)n_vec * kNearRT;
+  na.overwrite = (flags & FHTB_OVERWRITE) ? 1 : 0;
+  CU(launch_near(na, (int)tiles.size(), (int)q0.size() - 1, st));
+  CU(launch_near_reduce(d_rts, (int)rts.size(), part, F, ldf, n_vec, na.overwrite, st));
+  return FHTB_OK;
+}
+
+
+// ------------------------------------------------------------ DCT-I/DST-I
+// DCT-I: out[k] = Re sum_{m<n} v_m e^{i pi k m/(n-1)},  k < n   (trig.py:59-66)
+// DST-I: out[k] = Im sum_{m<n} v_m e^{i pi (k+1)(m+1)/(n+1)}    (trig.py:69-77)
+static int trig_geom(int kind, int64_t n, long long* L, long long* k0, int* logQ) {
+  if (kind == FHTB_DCT1) {
+    if (n < 2) return fail(FHTB_EINVAL, "DCT-I needs length >= 2");
+    *L = n - 1;
+    *k0 = 0;
+  } else if (kind == FHTB_DST1) {
+    if (n < 1) return fail(FHTB_EINVAL, "DST-I needs length >= 1");
+    *L = n + 1;
+    *k0 = 1;
+  } else {
+    return fail(FHTB_EINVAL, "kind must be DCT1 or DST1");
+  }
+  *logQ = std::max(1, ilog2ll(2 * n - 1));
+  if (*logQ > 13) return fail(FHTB_EINVAL, "trig_apply supports length <= 4096");
+  return FHTB_OK;
+}
+
+size_t fhtb_trig_workspace(int kind, int64_t length, int64_t batch) {
+  (void)batch;
+  long long L, k0;
+  int lq;
+  if (trig_geom(kind, length, &L, &k0, &lq)) return 0;
+  return 3 * align_up(sizeof(double2) << lq) + 4096;
+}
+
+int fhtb_trig_apply(int kind, int64_t length, const double* v, int64_t batch, double* out, void* ws,
+                    size_t ws_bytes, void* stream) {
+  long long L, k0;
+  int lq;
+  if (int r = trig_geom(kind, length, &L, &k0, &lq)) return r;
+  if (batch == 0) return FHTB_OK;
+  if (ws_bytes < fhtb_trig_workspace(kind, length, batch)) return fail(FHTB_EINVAL, "workspace too small");
+  DevCtx* ctx;
+  if (int r = get_ctx(&ctx)) return r;
+  cudaStream_t st = S(stream);
+  Carve cv{(char*)ws, ws_bytes};
+  const long long Q = 1LL << lq;
+  double2* h = cv.take<double2>(Q);
+  double2* tmp = cv.take<double2>(Q);
+  double2* H = cv.take<double2>(Q);
+  CU(launch_chirp_filter(h, Q, length, length, 1, L, st));
+  if (int r = plain_fft(ctx, lq, h, tmp, H, st)) return r;
+  CU(launch_trig(kind, lq, length, L, k0, k0, v, out, batch, H, ctx->tw, st));
+  return FHTB_OK;
+}
+
+}  // extern "C"

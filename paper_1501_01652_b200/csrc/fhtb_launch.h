@@ -1,0 +1,103 @@
+// fhtb_launch.h -- kernel argument blocks and launch entry points
+// (implemented in fhtb_*.cu, called from the host runtime fhtb_host.cpp).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "fhtb_types.h"
+
+namespace fhtb {
+
+struct JOrder;
+
+struct NearRowTile {
+  long long j0;
+  int nrows;
+  int nchunks;
+  long long part;
+};
+
+struct NearArgs {
+  const NearTile* tiles;
+  long long first, stride;      // output index j -> grid row k = first + stride*j
+  const double* rowv;           // null: row factor k; else rowv[k-1]
+  const double* colv;           // null: column factor (n+gamma)*scale; else colv[n-1]
+  double gamma, scale, Ld;
+  int n_orders, omax;
+  int orders[kMaxOrd];
+  const JOrder* jtab;           // indexed by order
+  const ReqDesc* reqs;
+  const int* grp_q0;            // requests of group g: [grp_q0[g], grp_q0[g+1])
+  const int* grp_v0;            // vectors of group g
+  const double* C;
+  long long ldc, n_data_cols;
+  double* F;
+  long long ldf;
+  double* part;
+  long long part_stride;         // n_vec * 64 doubles per partial slot
+  int overwrite;
+};
+
+struct FarArgs {
+  long long L;                  // grid length
+  int L1, L2;                   // FFT split: Q = L1 * L2 (2L in direct mode)
+  int M;                        // term pairs (direct) / 2M terms (chirp)
+  int logQ;
+  double gamma, Ld, pi_over_L;
+  long long first, stride;      // output rows
+  long long n_out;
+  long long n_data_cols;
+  const UnitDesc* units;
+  const ReqDesc* reqs;
+  const BlockDesc* blocks;
+  const int2* vranges;          // unit ranges per grid.y
+  int u0;                       // first unit of the chunk (G is indexed by unit - u0)
+  const double* C;
+  long long ldc;
+  double* F;
+  long long ldf;
+  double2* G;                   // intermediate
+  double* part;                 // chirp mode: per-unit partial rows
+  long long part_stride;
+  const double2* tw;            // twiddle pool: table for N at offset N-2
+  const double2* qlo;           // four-step twiddles e^{2 pi i m / Q}, m = hi*4096 + lo
+  const double2* qhi;
+  int qbits;                    // number of lo bits (<= 12)
+};
+
+cudaError_t launch_near(const NearArgs& a, int n_tiles, int n_groups, cudaStream_t st);
+cudaError_t launch_near_reduce(const NearRowTile* rt, int n_rt, const double* part, double* F,
+                               long long ldf, int n_vec, int overwrite, cudaStream_t st);
+constexpr int kNearRT = 64;
+
+// direct mode (2L power of two, unit-stride rows)
+cudaError_t launch_far_onepass(const FarArgs& a, int logN1, int n_ranges, cudaStream_t st);
+cudaError_t launch_far_pass1(const FarArgs& a, int logN2, int n_units, cudaStream_t st);
+cudaError_t launch_far_pass2(const FarArgs& a, int logN1, cudaStream_t st);
+
+// chirp mode (any grid length, strided output rows)
+cudaError_t launch_chirp_pass1(const FarArgs& a, int logN2, int n_units, cudaStream_t st);
+cudaError_t launch_chirp_pass2(const FarArgs& a, int logN1, int n_units, cudaStream_t st);
+cudaError_t launch_chirp_pass3(const FarArgs& a, int logN2, int n_units, cudaStream_t st);
+cudaError_t launch_chirp_reduce(const FarArgs& a, int n_units, cudaStream_t st);
+cudaError_t launch_chirp_filter(double2* h, long long Q, long long Mn, long long J, long long s, long long L,
+                                cudaStream_t st);
+cudaError_t launch_plain_fft(const FarArgs& a, int logN1, int logN2, const double2* in, double2* tmp,
+                             double2* out, cudaStream_t st);
+cudaError_t launch_trig(int kind, int logQ, long long n, long long L, long long k0, long long n0, const double* v,
+                        double* out, long long batch, const double2* H, const double2* tw, cudaStream_t st);
+
+// utilities
+cudaError_t launch_twiddles(double2* tw_pool, int max_log, cudaStream_t st);
+cudaError_t launch_qtwiddles(double2* qlo, double2* qhi, int logQ, int qbits, int sign, cudaStream_t st);
+cudaError_t launch_bessel_j(int nu, const JOrder& c, const double* z, long long n, double* out, cudaStream_t st);
+cudaError_t launch_bessel_multi(int omax, const JOrder* tab, const double* z, long long n, double* out, cudaStream_t st);
+cudaError_t launch_hankel_eval(int nu, int m_terms, const double* coef, const double* z, long long n,
+                               double* out, cudaStream_t st);
+cudaError_t launch_taylor_eval(int nu, int n_terms, double inv_fact, const double* z, long long n,
+                               double* out, cudaStream_t st);
+cudaError_t launch_roots_j0(const JOrder* tab, long long count, double* roots, double* pert,
+                            unsigned long long* resid_bits, cudaStream_t st);
+cudaError_t launch_fft_batch(int logN, int sign, const double2* in, double2* out, long long batch,
+                             const double2* tw_pool, cudaStream_t st);
+
+}  // namespace fhtb

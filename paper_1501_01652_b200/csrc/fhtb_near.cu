@@ -1,0 +1,208 @@
+// fhtb_near.cu -- near-field ("border") and direct-summation kernel.
+//
+//   out[vec][j] (+)= post_q(k) * sum_n sum_o w_q[o] J_o(rowf(k) * colf(n)) x_q[n]
+//
+// over a list of tiles (output rows x grid columns).  This single kernel is
+// the GPU form of
+//   * the Schlomilch border  _eval_segments / SchlomilchEngine._mask_streamed
+//     (schlomilch.py:193-220, 504-531),
+//   * schlomilch_direct (schlomilch.py:223-229),
+//   * the Fourier-Bessel low columns _direct_columns_many
+//     (fourier_bessel.py:148-172),
+//   * the DHT direct rows _rows_direct (dht.py:82-94).
+//
+// Bessel values are generated in registers (one Miller sweep yields every
+// order of the universe), staged in shared memory, and contracted against
+// the weighted coefficient tile with fp64 tensor-core MMA (wmma m8n8k4 ->
+// DMMA).  The reduction order over columns is fixed, so results are
+// reproducible run to run.
+#include <mma.h>
+
+#include "fhtb_bessel.cuh"
+#include "fhtb_core.cuh"
+#include "fhtb_launch.h"
+
+namespace fhtb {
+
+using namespace nvcuda;
+
+constexpr int kRT = kNearRT;   // output rows per tile
+constexpr int kJT = 64;        // request columns per CTA
+constexpr int kNearThreads = 256;
+
+template <int NORD> struct NearCfg {
+  static constexpr int NK = NORD <= 2 ? 16 : (NORD <= 4 ? 8 : 4);   // grid columns per step
+  static constexpr int K = NK * NORD;                                // MMA depth per step
+  static constexpr int A_ELEMS = kRT * K;
+  static constexpr int B_ELEMS = K * kJT;
+  static constexpr int C_ELEMS = kRT * kJT;
+  static constexpr int SMEM = 8 * ((A_ELEMS + B_ELEMS) > C_ELEMS ? (A_ELEMS + B_ELEMS) : C_ELEMS);
+};
+
+__device__ __forceinline__ double ipow(double x, int p) {
+  double r = 1.0;
+  for (int i = 0; i < p; ++i) r *= x;
+  return r;
+}
+
+template <int NORD>
+__global__ void __launch_bounds__(kNearThreads)
+near_kernel(NearArgs a) {
+  using Cfg = NearCfg<NORD>;
+  constexpr int NK = Cfg::NK, K = Cfg::K;
+  extern __shared__ double smem[];
+  double* As = smem;                       // [kRT][K]
+  double* Bs = smem + Cfg::A_ELEMS;        // [K][kJT]
+  double* Cs = smem;                       // [kRT][kJT] (epilogue, aliases As/Bs)
+
+  const NearTile tile = a.tiles[blockIdx.x];
+  const int g = blockIdx.y;
+  const int q0 = a.grp_q0[g], q1 = a.grp_q0[g + 1];
+  const int nq = q1 - q0;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+
+  wmma::fragment<wmma::accumulator, 8, 8, 4, double> acc[kJT / 8];
+#pragma unroll
+  for (int f = 0; f < kJT / 8; ++f) wmma::fill_fragment(acc[f], 0.0);
+  const int nfrag = (nq + 7) >> 3;
+
+  for (long long n0 = tile.na; n0 < tile.nb; n0 += NK) {
+    // ---- Bessel tile: As[i][u*NK + q] = J_{orders[u]}(z_{i,q})
+    for (int e = tid; e < kRT * NK; e += kNearThreads) {
+      const int i = e / NK, q = e % NK;
+      const long long n = n0 + q;
+      const long long j = tile.j0 + i;
+      double vals[NORD];
+#pragma unroll
+      for (int u = 0; u < NORD; ++u) vals[u] = 0.0;
+      if (i < tile.nrows && n < tile.nb) {
+        const long long k = a.first + a.stride * j;
+        const double rf = a.rowv ? a.rowv[k - 1] : (double)k;
+        const double cf = a.colv ? a.colv[n - 1] : ((double)n + a.gamma) * a.scale;
+        const double z = rf * cf;
+        if (NORD == 1) {
+          vals[0] = jn(a.orders[0], z, a.jtab[a.orders[0]]);
+        } else {
+          double all[kMaxOrd];
+          jn_all<kMaxOrd>(a.omax, z, a.jtab, all);
+#pragma unroll
+          for (int u = 0; u < NORD; ++u)
+            if (u < a.n_orders) {
+              double v = 0.0;
+#pragma unroll
+              for (int o = 0; o < kMaxOrd; ++o)
+                if (o == a.orders[u]) v = all[o];
+              vals[u] = v;
+            }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < NORD; ++u) As[i * K + u * NK + q] = vals[u];
+    }
+    // ---- weighted coefficient tile: Bs[u*NK + q][c] = w_c[u] * x_c[n]
+    for (int e = tid; e < NK * kJT; e += kNearThreads) {
+      const int q = e / kJT, c = e % kJT;
+      const long long n = n0 + q;
+      double x = 0.0;
+      const ReqDesc* r = nullptr;
+      if (c < nq && n < tile.nb) {
+        r = a.reqs + q0 + c;
+        if (n >= r->col_lo && n <= a.n_data_cols) {
+          x = a.C[(long long)r->vec * a.ldc + (n - 1)];
+          if (r->preA) x *= ipow(r->preA[n - 1], r->pa);
+          if (r->preB) x *= ipow(r->preB[n - 1], r->pb);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < NORD; ++u) Bs[(u * NK + q) * kJT + c] = r ? r->w[u] * x : 0.0;
+    }
+    __syncthreads();
+    // ---- DMMA: warp w owns rows [8w, 8w+8)
+#pragma unroll
+    for (int kk = 0; kk < K / 4; ++kk) {
+      wmma::fragment<wmma::matrix_a, 8, 8, 4, double, wmma::row_major> fa;
+      wmma::load_matrix_sync(fa, As + (warp * 8) * K + kk * 4, K);
+#pragma unroll
+      for (int f = 0; f < kJT / 8; ++f) {
+        if (f < nfrag) {
+          wmma::fragment<wmma::matrix_b, 8, 8, 4, double, wmma::row_major> fb;
+          wmma::load_matrix_sync(fb, Bs + (kk * 4) * kJT + f * 8, kJT);
+          wmma::mma_sync(acc[f], fa, fb, acc[f]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // ---- epilogue: reduce request columns into vectors with post factors
+#pragma unroll
+  for (int f = 0; f < kJT / 8; ++f)
+    wmma::store_matrix_sync(Cs + (warp * 8) * kJT + f * 8, acc[f], kJT, wmma::mem_row_major);
+  __syncthreads();
+  const int v0 = a.grp_v0[g], v1 = a.grp_v0[g + 1];
+  const int nv = v1 - v0;
+  for (int e = tid; e < kRT * nv; e += kNearThreads) {
+    const int i = e % kRT, vl = e / kRT;
+    if (i >= tile.nrows) continue;
+    const int vec = v0 + vl;
+    const long long j = tile.j0 + i;
+    const long long k = a.first + a.stride * j;
+    double s = 0.0;
+    for (int c = 0; c < nq; ++c) {
+      const ReqDesc* r = a.reqs + q0 + c;
+      if (r->vec != vec) continue;
+      double p = Cs[i * kJT + c];
+      if (r->pr) p *= ipow((double)k / a.Ld, r->pr);
+      if (r->post_e && r->pe) p *= ipow(r->post_e[j], r->pe);
+      s += p;
+    }
+    if (tile.part >= 0) {
+      a.part[tile.part * a.part_stride + (long long)vec * kRT + i] = s;
+    } else {
+      double* dst = a.F + (long long)vec * a.ldf + j;
+      *dst = a.overwrite ? s : *dst + s;
+    }
+  }
+}
+
+// Sum column-chunk partials of one row tile in chunk order.
+__global__ void near_reduce_kernel(const NearRowTile* rt, const double* part, double* F,
+                                   long long ldf, int n_vec, int overwrite) {
+  const NearRowTile t = rt[blockIdx.x];
+  for (int e = threadIdx.x; e < kRT * n_vec; e += blockDim.x) {
+    const int i = e % kRT, v = e / kRT;
+    if (i >= t.nrows) continue;
+    double s = 0.0;
+    for (int c = 0; c < t.nchunks; ++c)
+      s += part[(t.part + c) * (long long)n_vec * kRT + (long long)v * kRT + i];
+    double* dst = F + (long long)v * ldf + t.j0 + i;
+    *dst = overwrite ? s : *dst + s;
+  }
+}
+
+template <int NORD>
+static cudaError_t launch_near_t(const NearArgs& a, int n_tiles, int n_groups, cudaStream_t st) {
+  constexpr int smem = NearCfg<NORD>::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(near_kernel<NORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  near_kernel<NORD><<<dim3(n_tiles, n_groups), kNearThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_near(const NearArgs& a, int n_tiles, int n_groups, cudaStream_t st) {
+  if (n_tiles == 0 || n_groups == 0) return cudaSuccess;
+  if (a.n_orders <= 1) return launch_near_t<1>(a, n_tiles, n_groups, st);
+  if (a.n_orders <= 2) return launch_near_t<2>(a, n_tiles, n_groups, st);
+  if (a.n_orders <= 4) return launch_near_t<4>(a, n_tiles, n_groups, st);
+  if (a.n_orders <= 8) return launch_near_t<8>(a, n_tiles, n_groups, st);
+  return launch_near_t<16>(a, n_tiles, n_groups, st);
+}
+
+cudaError_t launch_near_reduce(const NearRowTile* rt, int n_rt, const double* part, double* F,
+                               long long ldf, int n_vec, int overwrite, cudaStream_t st) {
+  if (n_rt == 0) return cudaSuccess;
+  near_reduce_kernel<<<n_rt, 256, 0, st>>>(rt, part, F, ldf, n_vec, overwrite);
+  return cudaGetLastError();
+}
+
+}  // namespace fhtb
