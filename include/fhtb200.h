@@ -36,6 +36,8 @@ extern "C" {
 
 int fhtb_abi_version(void);
 const char* fhtb_last_error(void);
+/* Cumulative number of CUDA kernels this library has launched (all devices). */
+int64_t fhtb_launch_count(void);
 /* Prepare per-device tables (twiddles, Bessel order constants) on the
  * current device.  Idempotent; synchronous. */
 int fhtb_init(void);

@@ -78,9 +78,10 @@ def as_real_batch(c):
     (the transforms are real-linear, test_schlomilch.py:256-264).
     """
     is_torch = isinstance(c, torch.Tensor)
+    host_tensor = is_torch and c.device.type == "cpu"
     if is_torch:
         cplx = c.is_complex()
-        arr = c
+        arr = c.to(device(), non_blocking=True) if host_tensor else c
     else:
         arr = np.asarray(c)
         cplx = np.iscomplexobj(arr)
@@ -102,7 +103,7 @@ def as_real_batch(c):
             realt = to_dev_f64(both, dev)
     else:
         realt = to_dev_f64(arr.reshape(-1, arr.shape[-1]) if not is_torch else arr.reshape(-1, arr.shape[-1]), dev)
-    return realt, dict(torch=is_torch, complex=cplx, one=one)
+    return realt, dict(torch=is_torch, host_tensor=host_tensor, complex=cplx, one=one)
 
 
 def from_real_batch(F, meta):
@@ -112,6 +113,10 @@ def from_real_batch(F, meta):
         F = torch.complex(F[:, 0], F[:, 1])
     if meta["one"]:
         F = F[0]
+    if meta.get("host_tensor"):
+        out = torch.empty(F.shape, dtype=F.dtype, pin_memory=True)
+        out.copy_(F, non_blocking=False)
+        return out
     if meta["torch"]:
         return F
     return F.cpu().numpy()

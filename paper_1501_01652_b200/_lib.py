@@ -44,6 +44,7 @@ class DirectDesc(ctypes.Structure):
 EXPORTS = {
     "fhtb_abi_version": (i32, []),
     "fhtb_last_error": (ctypes.c_char_p, []),
+    "fhtb_launch_count": (i64, []),
     "fhtb_init": (i32, []),
     "fhtb_set_option": (i32, [ctypes.c_char_p, i64]),
     "fhtb_bessel_j": (i32, [i32, vp, i64, vp, vp]),

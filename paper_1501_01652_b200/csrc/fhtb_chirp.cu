@@ -246,7 +246,7 @@ __global__ void chirp_reduce_kernel(FarArgs a, int n_units) {
 
 cudaError_t launch_chirp_reduce(const FarArgs& a, int n_units, cudaStream_t st) {
   const long long b = (a.n_out + 255) / 256;
-  chirp_reduce_kernel<<<(unsigned)b, 256, 0, st>>>(a, n_units);
+  note_launch(), chirp_reduce_kernel<<<(unsigned)b, 256, 0, st>>>(a, n_units);
   return cudaGetLastError();
 }
 
@@ -360,7 +360,7 @@ static cudaError_t c1_w(const FarArgs& a, int n_units, cudaStream_t st) {
   auto k = chirp_pass1_kernel<N2, E, W>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k<<<dim3(a.L1 / W, n_units), W * (N2 / E), smem, st>>>(a);
+  note_launch(), k<<<dim3(a.L1 / W, n_units), W * (N2 / E), smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -372,7 +372,7 @@ static cudaError_t c3_w(const FarArgs& a, int n_ranges, cudaStream_t st) {
   auto k = chirp_pass3_kernel<N2, E, W>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k<<<dim3(a.L1 / W, n_ranges), W * (N2 / E), smem, st>>>(a);
+  note_launch(), k<<<dim3(a.L1 / W, n_ranges), W * (N2 / E), smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -384,7 +384,7 @@ static cudaError_t pp1_w(const double2* in, double2* out, const FarArgs& a, cuda
   auto k = plain_pass1_kernel<N2, E, W, S>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k<<<dim3(a.L1 / W), W * (N2 / E), smem, st>>>(in, out, a);
+  note_launch(), k<<<dim3(a.L1 / W), W * (N2 / E), smem, st>>>(in, out, a);
   return cudaGetLastError();
 }
 
@@ -430,7 +430,7 @@ static cudaError_t c2_t(const FarArgs& a, int n_units, cudaStream_t st) {
   auto k = chirp_pass2_kernel<N1, E>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k<<<dim3(a.L2, n_units), N1 / E, smem, st>>>(a);
+  note_launch(), k<<<dim3(a.L2, n_units), N1 / E, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -448,7 +448,7 @@ static cudaError_t pp2_t(const double2* in, double2* out, const FarArgs& a, cuda
   auto k = plain_pass2_kernel<N1, E, S>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k<<<dim3(a.L2), N1 / E, smem, st>>>(in, out, a);
+  note_launch(), k<<<dim3(a.L2), N1 / E, smem, st>>>(in, out, a);
   return cudaGetLastError();
 }
 
@@ -493,7 +493,7 @@ cudaError_t launch_chirp_filter(double2* h, long long Q, long long Mn, long long
                                 cudaStream_t st) {
   long long b = (Q + 255) / 256;
   if (b > 148 * 64) b = 148 * 64;
-  chirp_filter_kernel<<<(int)b, 256, 0, st>>>(h, Q, Mn, J, s, L);
+  note_launch(), chirp_filter_kernel<<<(int)b, 256, 0, st>>>(h, Q, Mn, J, s, L);
   return cudaGetLastError();
 }
 
@@ -505,7 +505,7 @@ static cudaError_t trig_t(int kind, long long n, long long L, long long k0, long
   auto k = trig_kernel<N, E>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k<<<(unsigned)batch, N / E, smem, st>>>(kind, n, L, k0, n0, v, out, H, tw);
+  note_launch(), k<<<(unsigned)batch, N / E, smem, st>>>(kind, n, L, k0, n0, v, out, H, tw);
   return cudaGetLastError();
 }
 

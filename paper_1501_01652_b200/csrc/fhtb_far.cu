@@ -255,7 +255,7 @@ static cudaError_t p1_t(const FarArgs& a, int n_units, cudaStream_t st) {
   auto k = far_pass1_kernel<N2, E, W>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k<<<dim3(a.L1 / W, n_units), W * T, smem, st>>>(a);
+  note_launch(), k<<<dim3(a.L1 / W, n_units), W * T, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -269,7 +269,7 @@ static cudaError_t p2_t(const FarArgs& a, int gx, int gy, cudaStream_t st) {
   auto k = far_pass2_kernel<N1, E, ONE>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k<<<dim3(gx, gy), NCOL * T, smem, st>>>(a);
+  note_launch(), k<<<dim3(gx, gy), NCOL * T, smem, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -6,6 +6,7 @@
 // near-field tiling and vector grouping.  All scheduling decisions are
 // deterministic functions of the arguments, so results are reproducible.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -19,6 +20,11 @@
 #include "fhtb_launch.h"
 
 using namespace fhtb;
+
+namespace fhtb {
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace fhtb
 
 namespace {
 
@@ -344,6 +350,7 @@ int plain_fft(DevCtx* ctx, int logQ, const double2* in, double2* tmp, double2* o
 extern "C" {
 
 int fhtb_abi_version(void) { return 1; }
+int64_t fhtb_launch_count(void) { return g_launches.load(); }
 const char* fhtb_last_error(void) { return g_err.c_str(); }
 
 int fhtb_init(void) {

@@ -7,6 +7,9 @@
 
 namespace fhtb {
 
+// Cumulative count of kernels launched by the library (fhtb_launch_count).
+void note_launch();
+
 struct JOrder;
 
 struct NearRowTile {

@@ -147,8 +147,8 @@ template <int N>
 static cudaError_t fftb_t(int sign, const double2* in, double2* out, long long batch,
                           const double2* tw, cudaStream_t st) {
   constexpr int E = N >= 16 ? 16 : N;
-  if (sign > 0) fft_batch_kernel<N, 1><<<(unsigned)batch, N / E, 0, st>>>(in, out, tw);
-  else fft_batch_kernel<N, -1><<<(unsigned)batch, N / E, 0, st>>>(in, out, tw);
+  if (sign > 0) note_launch(), fft_batch_kernel<N, 1><<<(unsigned)batch, N / E, 0, st>>>(in, out, tw);
+  else note_launch(), fft_batch_kernel<N, -1><<<(unsigned)batch, N / E, 0, st>>>(in, out, tw);
   return cudaGetLastError();
 }
 
@@ -172,46 +172,46 @@ cudaError_t launch_fft_batch(int logN, int sign, const double2* in, double2* out
 
 cudaError_t launch_twiddles(double2* pool, int max_log, cudaStream_t st) {
   const long long total = (1LL << (max_log + 1)) - 2;
-  twiddle_kernel<<<grid_for(total, 256), 256, 0, st>>>(pool, max_log);
+  note_launch(), twiddle_kernel<<<grid_for(total, 256), 256, 0, st>>>(pool, max_log);
   return cudaGetLastError();
 }
 
 cudaError_t launch_qtwiddles(double2* qlo, double2* qhi, int logQ, int qbits, int sign, cudaStream_t st) {
   const long long n = (1LL << qbits) + ((1LL << logQ) >> qbits);
-  qtwiddle_kernel<<<grid_for(n, 256), 256, 0, st>>>(qlo, qhi, logQ, qbits, sign);
+  note_launch(), qtwiddle_kernel<<<grid_for(n, 256), 256, 0, st>>>(qlo, qhi, logQ, qbits, sign);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bessel_j(int nu, const JOrder& c, const double* z, long long n, double* out, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  bessel_j_kernel<<<grid_for(n, 256), 256, 0, st>>>(nu, c, z, n, out);
+  note_launch(), bessel_j_kernel<<<grid_for(n, 256), 256, 0, st>>>(nu, c, z, n, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bessel_multi(int omax, const JOrder* tab, const double* z, long long n, double* out,
                                 cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  bessel_multi_kernel<<<grid_for(n, 256), 256, 0, st>>>(omax, tab, z, n, out);
+  note_launch(), bessel_multi_kernel<<<grid_for(n, 256), 256, 0, st>>>(omax, tab, z, n, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_hankel_eval(int nu, int mt, const double* coef, const double* z, long long n, double* out,
                                cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  hankel_eval_kernel<<<grid_for(n, 256), 256, 0, st>>>(nu, mt, coef, z, n, out);
+  note_launch(), hankel_eval_kernel<<<grid_for(n, 256), 256, 0, st>>>(nu, mt, coef, z, n, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_taylor_eval(int nu, int nt, double inv_fact, const double* z, long long n, double* out,
                                cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  taylor_eval_kernel<<<grid_for(n, 256), 256, 0, st>>>(nu, nt, inv_fact, z, n, out);
+  note_launch(), taylor_eval_kernel<<<grid_for(n, 256), 256, 0, st>>>(nu, nt, inv_fact, z, n, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_roots_j0(const JOrder* tab, long long count, double* roots, double* pert,
                             unsigned long long* resid_bits, cudaStream_t st) {
-  roots_j0_kernel<<<grid_for(count, 256), 256, 0, st>>>(tab, count, roots, pert, resid_bits);
+  note_launch(), roots_j0_kernel<<<grid_for(count, 256), 256, 0, st>>>(tab, count, roots, pert, resid_bits);
   return cudaGetLastError();
 }
 

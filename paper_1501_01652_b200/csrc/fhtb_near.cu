@@ -185,7 +185,7 @@ static cudaError_t launch_near_t(const NearArgs& a, int n_tiles, int n_groups, c
   constexpr int smem = NearCfg<NORD>::SMEM;
   cudaError_t e = cudaFuncSetAttribute(near_kernel<NORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  near_kernel<NORD><<<dim3(n_tiles, n_groups), kNearThreads, smem, st>>>(a);
+  note_launch(), near_kernel<NORD><<<dim3(n_tiles, n_groups), kNearThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -201,7 +201,7 @@ cudaError_t launch_near(const NearArgs& a, int n_tiles, int n_groups, cudaStream
 cudaError_t launch_near_reduce(const NearRowTile* rt, int n_rt, const double* part, double* F,
                                long long ldf, int n_vec, int overwrite, cudaStream_t st) {
   if (n_rt == 0) return cudaSuccess;
-  near_reduce_kernel<<<n_rt, 256, 0, st>>>(rt, part, F, ldf, n_vec, overwrite);
+  note_launch(), near_reduce_kernel<<<n_rt, 256, 0, st>>>(rt, part, F, ldf, n_vec, overwrite);
   return cudaGetLastError();
 }
 
