@@ -15,15 +15,17 @@
 // (L/k)^{i+1/2}, the gamma-shift diagonals cos/sin(theta_k + (2o+1)pi/4)
 // (Remark 1), the order combination (schlomilch.py:280-299) and the
 // post-multipliers r^u / e^u (fourier_bessel.py:240-242, dht.py:167-174) are
-// applied in the epilogue of the last FFT pass, which accumulates all units
-// of one coefficient vector in registers and writes the output once.
+// applied in the epilogue of the last FFT pass, which reduces all 2M terms
+// of a (request, block) unit in registers and writes one partial row.
 //
-//   one-pass  (2L <= 8192): one CTA per vector, whole FFT in shared memory.
+//   one-pass  (2L <= 8192): one CTA per unit, whole FFT in shared memory.
 //   two-pass  (2L  > 8192): Q = 2L = L1*L2 four-step.
 //      pass 1: per column n1, L2-point FFT over n2 (n = n1 + L1 n2), twiddle
 //              e^{2 pi i n1 k2 / Q}, store G[unit][p][k2][n1].
-//      pass 2: per column pair {k2, L2-k2}, L1-point FFTs over n1, then the
-//              fused DCT/DST separation + row epilogue.
+//      pass 2: per (column pair {k2, L2-k2}, unit), L1-point FFTs over n1,
+//              the fused DCT/DST separation and the row epilogue.
+//   reduce:  F[vec][j] += sum of the unit partials of that vector, in unit
+//            order (deterministic).
 #include "fhtb_core.cuh"
 #include "fhtb_launch.h"
 
@@ -67,8 +69,8 @@ __device__ __forceinline__ void unit_cols(const FarArgs& a, const ReqDesc& R, co
 }
 
 // ------------------------------------------------------------------ pass 1
-template <int N2, int E, int W>
-__global__ void __launch_bounds__(W * (N2 / E))
+template <int N2, int E, int W, int MINB>
+__global__ void __launch_bounds__(W * (N2 / E), MINB)
 far_pass1_kernel(FarArgs a) {
   constexpr int T = N2 / E;
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
@@ -110,8 +112,8 @@ far_pass1_kernel(FarArgs a) {
 // --------------------------------------------- pass 2 / one-pass epilogue
 //
 // ONEPASS: L2 == 1, N1 == 2L, one column, input generated from c.
-template <int N1, int E, bool ONEPASS>
-__global__ void __launch_bounds__((ONEPASS ? 1 : 2) * (N1 / E))
+template <int N1, int E, bool ONEPASS, int MINB>
+__global__ void __launch_bounds__((ONEPASS ? 1 : 2) * (N1 / E), MINB)
 far_pass2_kernel(FarArgs a) {
   constexpr int T = N1 / E;
   constexpr int NCOL = ONEPASS ? 1 : 2;
@@ -121,202 +123,246 @@ far_pass2_kernel(FarArgs a) {
   constexpr int NP = N1 + 4;
   constexpr int LOGE = ilog2c(E);
   extern __shared__ double2 sm2[];
-  double2* cs = sm2 + NCOL * NP;               // per-slot (cos theta, sin theta)
   const int tid = threadIdx.x, h = tid / T, tt = tid % T;
-  const long long L = a.L;
+  const int L = (int)a.L;
   const int L2 = a.L2;
   const int k2a = blockIdx.x, k2b = (L2 - k2a) % L2;
   const bool selfp = (k2a == k2b);
   const int myk2 = h == 0 ? k2a : k2b;
-  const int2 vr = a.vranges[blockIdx.y];
+  const int ul = blockIdx.y;
+  const UnitDesc U = a.units[a.u0 + ul];
+  const ReqDesc& R = a.reqs[U.req];
+  const BlockDesc& B = a.blocks[U.block];
   const double2* tw = a.tw + (N1 - 2);
 
-  // slot geometry
-  long long kq[NQ];
+  // slot geometry and row weights rp = post(k) (L/k)^{1/2} inside the block
+  int kq[NQ];
+  double acc[NQ], rp[NQ], ir[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int o = tid + NT * q;
     const int hh = o / HALF, qq = o % HALF;
-    long long k = 0;
+    int k = 0;
     if (hh < NCOL && !(selfp && hh == 1)) {
       const int k2 = hh == 0 ? k2a : k2b;
       const int k1 = (k2 == 0) ? qq + 1 : qq;
-      k = k2 + (long long)L2 * k1;
-      if (k < 1 || k > L) k = 0;
+      k = k2 + L2 * k1;
+      if (k < 1 || k > L || k < B.r0 || k >= B.r1) k = 0;
     }
     kq[q] = k;
-    double s = 0.0, c = 1.0;
-    if (k && a.gamma != 0.0) sincos(-a.gamma * (double)k * a.pi_over_L, &s, &c);
-    cs[o] = make_double2(c, s);
+    acc[q] = rp[q] = ir[q] = 0.0;
+    if (k) {
+      const double irk = a.Ld / (double)k;
+      double post = 1.0;
+      if (R.pr) post = ipow_f((double)k / a.Ld, R.pr);
+      if (R.post_e && R.pe) post *= ipow_f(R.post_e[k - 1], R.pe);
+      ir[q] = irk;
+      rp[q] = post * sqrt(irk);
+    }
   }
-  double acc[NQ], rp[NQ], ir[NQ];
+  double v[E], iw[E];
+  if (ONEPASS) {
+    long long cA, cB;
+    unit_cols(a, R, B, cA, cB);
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-
-  for (int u = vr.x; u < vr.y; ++u) {
-    const UnitDesc U = a.units[u];
-    const ReqDesc& R = a.reqs[U.req];
-    const BlockDesc& B = a.blocks[U.block];
-    // per-slot row weights: rp = post(k) * (L/k)^{1/2} inside the block rows
+    for (int e = 0; e < E; ++e) load_col(a, R, cA, cB, tt + T * e, v[e], iw[e]);
+  }
+  for (int p = 0; p < a.M; ++p) {
+    double2 z[E];
+    if (ONEPASS) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const double im = v[e] * iw[e];
+        z[e] = make_double2(v[e], im);
+        v[e] = im * iw[e];
+      }
+    } else {
+      const double2* G = a.G + ((long long)(ul * a.M + p) * L2 + myk2) * N1;
+#pragma unroll
+      for (int e = 0; e < E; ++e) z[e] = G[tt + T * e];
+    }
+    __syncthreads();
+    block_fft<N1, E, 1>(z, sm2 + h * NP, tt, tw);
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < E; ++s) sm2[h * NP + swz<LOGE>(fft_out_index<N1, E>(tt, s))] = z[s];
+    __syncthreads();
+    const int i0 = 2 * p, i1 = 2 * p + 1;
+    const double ac0 = R.ac[i0], as0 = R.as[i0], bc0 = R.bc[i0], bs0 = R.bs[i0];
+    const double ac1 = R.ac[i1], as1 = R.as[i1], bc1 = R.bc[i1], bs1 = R.bs[i1];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      const long long k = kq[q];
-      rp[q] = 0.0;
-      ir[q] = 0.0;
-      if (k && k >= B.r0 && k < B.r1) {
-        const double irk = a.Ld / (double)k;
-        const long long j = (k - a.first) / a.stride;
-        double post = 1.0;
-        if (R.pr) post = ipow_f((double)k / a.Ld, R.pr);
-        if (R.post_e && R.pe) post *= ipow_f(R.post_e[j], R.pe);
-        ir[q] = irk;
-        rp[q] = post * sqrt(irk);
+      const int k = kq[q];
+      if (!k) continue;
+      const int k2 = k & (L2 - 1);
+      const int k1 = k / L2;
+      const int hk = (k2 == k2a) ? 0 : 1;
+      const int kp = 2 * L - k;
+      const int k2p = kp & (L2 - 1);
+      const int k1p = kp / L2;
+      const int hp = (k2p == k2a) ? 0 : 1;
+      const double2 Zk = sm2[hk * NP + swz<LOGE>(k1)];
+      const double2 Zp = cconj(sm2[hp * NP + swz<LOGE>(k1p)]);
+      double2 Ya = make_double2(0.5 * (Zk.x + Zp.x), 0.5 * (Zk.y + Zp.y));
+      double2 Yb = make_double2(0.5 * (Zk.y - Zp.y), -0.5 * (Zk.x - Zp.x));
+      if (k == L) { Ya.y = 0.0; Yb.y = 0.0; }      // S u has no row N (schlomilch.py:314-316)
+      double A0 = ac0, B0 = bc0, A1 = ac1, B1 = bc1;
+      if (a.cs_tab) {
+        const double2 th = __ldg(a.cs_tab + (k - 1));
+        A0 = ac0 * th.x + as0 * th.y; B0 = bc0 * th.x + bs0 * th.y;
+        A1 = ac1 * th.x + as1 * th.y; B1 = bc1 * th.x + bs1 * th.y;
       }
+      const double r0 = rp[q], r1 = r0 * ir[q];
+      acc[q] += r0 * (A0 * Ya.x + B0 * Ya.y) + r1 * (A1 * Yb.x + B1 * Yb.y);
+      rp[q] = r1 * ir[q];
     }
-    double v[E], iw[E];
-    long long cA = 0, cB = 0;
-    if (ONEPASS) {
-      unit_cols(a, R, B, cA, cB);
+  }
+  double* part = a.part + (long long)ul * a.part_stride;
 #pragma unroll
-      for (int e = 0; e < E; ++e) load_col(a, R, cA, cB, tt + T * e, v[e], iw[e]);
-    }
-    for (int p = 0; p < a.M; ++p) {
-      double2 z[E];
-      if (ONEPASS) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const double im = v[e] * iw[e];
-          z[e] = make_double2(v[e], im);
-          v[e] = im * iw[e];
-        }
-      } else {
-        const double2* G = a.G + ((long long)((u - a.u0) * a.M + p) * L2 + myk2) * N1;
-#pragma unroll
-        for (int e = 0; e < E; ++e) z[e] = G[tt + T * e];
+  for (int q = 0; q < NQ; ++q)
+    if (kq[q]) part[kq[q] - 1] = acc[q];
+}
+
+// F[vec][j] += sum over the chunk's units of vec whose block holds row j,
+// in unit order.  Units of one vector are contiguous in the chunk.
+__global__ void far_reduce_kernel(FarArgs a, int n_units) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= a.n_out) return;
+  const long long k = a.first + a.stride * j;
+  int u = 0;
+  while (u < n_units) {
+    const int vec = a.units[a.u0 + u].vec;
+    double s = 0.0;
+    bool any = false;
+    while (u < n_units && a.units[a.u0 + u].vec == vec) {
+      const BlockDesc& B = a.blocks[a.units[a.u0 + u].block];
+      if (k >= B.r0 && k < B.r1) {
+        s += a.part[(long long)u * a.part_stride + j];
+        any = true;
       }
-      __syncthreads();
-      block_fft<N1, E, 1>(z, sm2 + h * NP, tt, tw);
-      __syncthreads();
-#pragma unroll
-      for (int s = 0; s < E; ++s) sm2[h * NP + swz<LOGE>(fft_out_index<N1, E>(tt, s))] = z[s];
-      __syncthreads();
-      const int i0 = 2 * p, i1 = 2 * p + 1;
-      const double ac0 = R.ac[i0], as0 = R.as[i0], bc0 = R.bc[i0], bs0 = R.bs[i0];
-      const double ac1 = R.ac[i1], as1 = R.as[i1], bc1 = R.bc[i1], bs1 = R.bs[i1];
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        if (rp[q] == 0.0) continue;
-        const long long k = kq[q];
-        const int k2 = (int)(k % L2);
-        const long long k1 = k / L2;
-        const int hk = (k2 == k2a) ? 0 : 1;
-        const long long kp = 2 * L - k;
-        const int k2p = (int)(kp % L2);
-        const long long k1p = kp / L2;
-        const int hp = (k2p == k2a) ? 0 : 1;
-        const double2 Zk = sm2[hk * NP + swz<LOGE>((int)k1)];
-        const double2 Zp = cconj(sm2[hp * NP + swz<LOGE>((int)k1p)]);
-        double2 Ya = make_double2(0.5 * (Zk.x + Zp.x), 0.5 * (Zk.y + Zp.y));
-        double2 Yb = make_double2(0.5 * (Zk.y - Zp.y), -0.5 * (Zk.x - Zp.x));
-        if (k == L) { Ya.y = 0.0; Yb.y = 0.0; }      // S u has no row N (schlomilch.py:314-316)
-        const double2 th = cs[tid + NT * q];
-        const double A0 = ac0 * th.x + as0 * th.y, B0 = bc0 * th.x + bs0 * th.y;
-        const double A1 = ac1 * th.x + as1 * th.y, B1 = bc1 * th.x + bs1 * th.y;
-        const double r0 = rp[q], r1 = r0 * ir[q];
-        acc[q] += r0 * (A0 * Ya.x + B0 * Ya.y) + r1 * (A1 * Yb.x + B1 * Yb.y);
-        rp[q] = r1 * ir[q];
-      }
+      ++u;
     }
-    // flush when the next unit belongs to another vector
-    const bool last = (u + 1 == vr.y) || (a.units[u + 1].vec != U.vec);
-    if (last) {
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        const long long k = kq[q];
-        if (k && ((k - a.first) % a.stride) == 0 && k >= a.first) {
-          const long long j = (k - a.first) / a.stride;
-          double* dst = a.F + (long long)U.vec * a.ldf + j;
-          *dst += acc[q];
-        }
-        acc[q] = 0.0;
-      }
-    }
+    if (any) a.F[(long long)vec * a.ldf + j] += s;
   }
 }
 
 // ---------------------------------------------------------------- launch
-template <int N2>
+int g_far_variant = 0;
+
+template <int N2, int E, int W, int MINB>
 static cudaError_t p1_t(const FarArgs& a, int n_units, cudaStream_t st) {
-  constexpr int E = N2 >= 16 ? 16 : N2;
-  constexpr int W = N2 >= 4096 ? 1 : 4096 / N2;
   constexpr int T = N2 / E;
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
   const int smem = W * (N2 + PAD) * 16;
-  auto k = far_pass1_kernel<N2, E, W>;
+  auto k = far_pass1_kernel<N2, E, W, MINB>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   note_launch(), k<<<dim3(a.L1 / W, n_units), W * T, smem, st>>>(a);
   return cudaGetLastError();
 }
 
-template <int N1, bool ONE>
+template <int N2>
+static cudaError_t p1_d(const FarArgs& a, int n_units, cudaStream_t st) {
+  constexpr int E = N2 >= 16 ? 16 : N2;
+  constexpr int W = N2 >= 4096 ? 1 : 4096 / N2;
+  return p1_t<N2, E, W, 1>(a, n_units, st);
+}
+
+template <int N1, int E, bool ONE, int MINB>
 static cudaError_t p2_t(const FarArgs& a, int gx, int gy, cudaStream_t st) {
-  constexpr int E = N1 >= 16 ? 16 : N1;
   constexpr int T = N1 / E;
   constexpr int NCOL = ONE ? 1 : 2;
-  constexpr int NQ = E / 2 > 0 ? E / 2 : 1;
-  const int smem = (NCOL * (N1 + 4) + NCOL * T * NQ) * 16;
-  auto k = far_pass2_kernel<N1, E, ONE>;
+  const int smem = NCOL * (N1 + 4) * 16;
+  auto k = far_pass2_kernel<N1, E, ONE, MINB>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   note_launch(), k<<<dim3(gx, gy), NCOL * T, smem, st>>>(a);
   return cudaGetLastError();
 }
 
+template <int N1, bool ONE>
+static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
+  constexpr int E = N1 >= 16 ? 16 : N1;
+  return p2_t<N1, E, ONE, 1>(a, gx, gy, st);
+}
+
 cudaError_t launch_far_pass1(const FarArgs& a, int logN2, int n_units, cudaStream_t st) {
   switch (logN2) {
-    case 6: return p1_t<64>(a, n_units, st);
-    case 7: return p1_t<128>(a, n_units, st);
-    case 8: return p1_t<256>(a, n_units, st);
-    case 9: return p1_t<512>(a, n_units, st);
-    case 10: return p1_t<1024>(a, n_units, st);
-    case 11: return p1_t<2048>(a, n_units, st);
-    case 12: return p1_t<4096>(a, n_units, st);
-    case 13: return p1_t<8192>(a, n_units, st);
+    case 6: return p1_d<64>(a, n_units, st);
+    case 7: return p1_d<128>(a, n_units, st);
+    case 8: return p1_d<256>(a, n_units, st);
+    case 9: return p1_d<512>(a, n_units, st);
+    case 10:
+      switch (g_far_variant & 15) {
+        case 1: return p1_t<1024, 16, 2, 2>(a, n_units, st);
+        case 2: return p1_t<1024, 8, 2, 2>(a, n_units, st);
+        case 3: return p1_t<1024, 8, 4, 1>(a, n_units, st);
+        default: return p1_d<1024>(a, n_units, st);
+      }
+    case 11: return p1_d<2048>(a, n_units, st);
+    case 12: return p1_d<4096>(a, n_units, st);
+    case 13: return p1_d<8192>(a, n_units, st);
   }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_far_pass2(const FarArgs& a, int logN1, cudaStream_t st) {
+cudaError_t launch_far_pass2(const FarArgs& a, int logN1, int n_units, cudaStream_t st) {
   const int gx = a.L2 / 2 + 1;
   switch (logN1) {
-    case 7: return p2_t<128, false>(a, gx, 1, st);
-    case 8: return p2_t<256, false>(a, gx, 1, st);
-    case 9: return p2_t<512, false>(a, gx, 1, st);
-    case 10: return p2_t<1024, false>(a, gx, 1, st);
-    case 11: return p2_t<2048, false>(a, gx, 1, st);
-    case 12: return p2_t<4096, false>(a, gx, 1, st);
+    case 7: return p2_d<128, false>(a, gx, n_units, st);
+    case 8: return p2_d<256, false>(a, gx, n_units, st);
+    case 9: return p2_d<512, false>(a, gx, n_units, st);
+    case 10: return p2_d<1024, false>(a, gx, n_units, st);
+    case 11:
+      switch ((g_far_variant >> 4) & 15) {
+        case 1: return p2_t<2048, 16, false, 2>(a, gx, n_units, st);
+        case 2: return p2_t<2048, 8, false, 1>(a, gx, n_units, st);
+        case 3: return p2_t<2048, 8, false, 2>(a, gx, n_units, st);
+        default: return p2_d<2048, false>(a, gx, n_units, st);
+      }
+    case 12: return p2_d<4096, false>(a, gx, n_units, st);
   }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_far_onepass(const FarArgs& a, int logN1, int n_ranges, cudaStream_t st) {
+cudaError_t launch_far_onepass(const FarArgs& a, int logN1, int n_units, cudaStream_t st) {
   switch (logN1) {
-    case 1: return p2_t<2, true>(a, 1, n_ranges, st);
-    case 2: return p2_t<4, true>(a, 1, n_ranges, st);
-    case 3: return p2_t<8, true>(a, 1, n_ranges, st);
-    case 4: return p2_t<16, true>(a, 1, n_ranges, st);
-    case 5: return p2_t<32, true>(a, 1, n_ranges, st);
-    case 6: return p2_t<64, true>(a, 1, n_ranges, st);
-    case 7: return p2_t<128, true>(a, 1, n_ranges, st);
-    case 8: return p2_t<256, true>(a, 1, n_ranges, st);
-    case 9: return p2_t<512, true>(a, 1, n_ranges, st);
-    case 10: return p2_t<1024, true>(a, 1, n_ranges, st);
-    case 11: return p2_t<2048, true>(a, 1, n_ranges, st);
-    case 12: return p2_t<4096, true>(a, 1, n_ranges, st);
-    case 13: return p2_t<8192, true>(a, 1, n_ranges, st);
+    case 1: return p2_d<2, true>(a, 1, n_units, st);
+    case 2: return p2_d<4, true>(a, 1, n_units, st);
+    case 3: return p2_d<8, true>(a, 1, n_units, st);
+    case 4: return p2_d<16, true>(a, 1, n_units, st);
+    case 5: return p2_d<32, true>(a, 1, n_units, st);
+    case 6: return p2_d<64, true>(a, 1, n_units, st);
+    case 7: return p2_d<128, true>(a, 1, n_units, st);
+    case 8: return p2_d<256, true>(a, 1, n_units, st);
+    case 9: return p2_d<512, true>(a, 1, n_units, st);
+    case 10: return p2_d<1024, true>(a, 1, n_units, st);
+    case 11: return p2_d<2048, true>(a, 1, n_units, st);
+    case 12: return p2_d<4096, true>(a, 1, n_units, st);
+    case 13: return p2_d<8192, true>(a, 1, n_units, st);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_far_reduce(const FarArgs& a, int n_units, cudaStream_t st) {
+  const long long b = (a.n_out + 255) / 256;
+  note_launch(), far_reduce_kernel<<<(unsigned)b, 256, 0, st>>>(a, n_units);
+  return cudaGetLastError();
+}
+
+__global__ void cs_table_kernel(double2* cs, long long L, double gamma, double pi_over_L) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < L; i += (long long)gridDim.x * blockDim.x) {
+    double s, c;
+    sincos(-gamma * (double)(i + 1) * pi_over_L, &s, &c);
+    cs[i] = make_double2(c, s);
+  }
+}
+
+cudaError_t launch_cs_table(double2* cs, long long L, double gamma, double pi_over_L, cudaStream_t st) {
+  long long b = (L + 255) / 256;
+  if (b > 148 * 64) b = 148 * 64;
+  note_launch(), cs_table_kernel<<<(unsigned)b, 256, 0, st>>>(cs, L, gamma, pi_over_L);
+  return cudaGetLastError();
 }
 
 }  // namespace fhtb

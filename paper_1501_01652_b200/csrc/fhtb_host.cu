@@ -307,6 +307,7 @@ struct fhtb_grid {
   std::vector<BlockDesc> bdesc;    // host copy (chirp parameters)
   std::vector<double2*> H;         // chirp filter spectra per block
   BlockDesc* d_blocks = nullptr;
+  double2* cs_tab = nullptr;       // (cos, sin)(-gamma k pi/L), k = 1..L, when gamma != 0
   // near field
   std::vector<NearTile> tiles;
   std::vector<NearRowTile> rts;
@@ -360,6 +361,10 @@ int fhtb_init(void) {
 
 int fhtb_set_option(const char* key, int64_t value) {
   if (!key) return fail(FHTB_EINVAL, "null key");
+  if (!std::strcmp(key, "far_variant")) {
+    g_far_variant = (int)value;
+    return FHTB_OK;
+  }
   if (!std::strcmp(key, "far_chunk_bytes")) {
     if (value < (1 << 20)) return fail(FHTB_EINVAL, "far_chunk_bytes too small");
     g_far_chunk_bytes = value;
@@ -523,6 +528,10 @@ int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
     CU(cudaMalloc(&g->d_blocks, g->bdesc.size() * sizeof(BlockDesc)));
     CU(cudaMemcpy(g->d_blocks, g->bdesc.data(), g->bdesc.size() * sizeof(BlockDesc), cudaMemcpyHostToDevice));
   }
+  if (g->gamma != 0.0) {
+    CU(cudaMalloc(&g->cs_tab, g->L * sizeof(double2)));
+    CU(launch_cs_table(g->cs_tab, g->L, g->gamma, M_PI / (double)g->L, 0));
+  }
   if (g->direct && g->logN2 > 0) {
     double2 *ql, *qh;
     int qb;
@@ -545,6 +554,7 @@ int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
 void fhtb_grid_destroy(fhtb_grid* g) {
   if (!g) return;
   cudaFree(g->d_blocks);
+  cudaFree(g->cs_tab);
   for (double2* h : g->H) cudaFree(h);
   cudaFree(g->d_tiles);
   cudaFree(g->d_rts);
@@ -590,23 +600,19 @@ void plan_far(const fhtb_grid* g, const std::vector<ReqDesc>& rs, FarPlan& fp) {
   if (g->direct) {
     fp.units = all;
     const long long nu = (long long)all.size();
-    if (g->logN2 == 0) {
-      long long u = 0;
-      while (u < nu) {
-        long long e = u;
-        while (e < nu && all[e].vec == all[u].vec) ++e;
-        fp.chunks.push_back(make_int2((int)u, (int)e));
-        fp.chunk_logq.push_back(g->logQ);
-        u = e;
-      }
-    } else {
-      const size_t ub = unit_bytes_q(g, g->logQ);
-      const long long cu = chunk_for(ub, nu);
-      for (long long u0 = 0; u0 < nu; u0 += cu) {
-        fp.chunks.push_back(make_int2((int)u0, (int)std::min(nu, u0 + cu)));
-        fp.chunk_logq.push_back(g->logQ);
-      }
-      if (nu) fp.g_bytes = ub * cu;
+    // one-pass: every unit in one launch; two-pass: chunks bounded by the
+    // intermediate budget.  Partial rows: one per unit of a launch.
+    const size_t ub = g->logN2 == 0 ? 0 : unit_bytes_q(g, g->logQ);
+    const size_t pb = sizeof(double) * (size_t)g->n_out;
+    const long long cu = g->logN2 == 0 ? std::max<long long>(nu, 1)
+                                       : chunk_for(ub + pb, nu);
+    for (long long u0 = 0; u0 < nu; u0 += cu) {
+      fp.chunks.push_back(make_int2((int)u0, (int)std::min(nu, u0 + cu)));
+      fp.chunk_logq.push_back(g->logQ);
+    }
+    if (nu) {
+      fp.g_bytes = ub * cu;
+      fp.part_bytes = pb * cu;
     }
     return;
   }
@@ -718,12 +724,15 @@ int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
       a.G = G;
       a.part = part;
       a.part_stride = g->n_out;
+      a.cs_tab = g->cs_tab;
       if (g->direct && g->logN2 == 0) {
         a.L1 = 1 << g->logN1;
         a.L2 = 1;
         a.logQ = g->logQ;
         a.vranges = d_ch;
-        CU(launch_far_onepass(a, g->logN1, (int)fp.chunks.size(), st));
+        a.u0 = 0;
+        CU(launch_far_onepass(a, g->logN1, (int)nu, st));
+        CU(launch_far_reduce(a, (int)nu, st));
       } else {
         for (size_t ci = 0; ci < fp.chunks.size(); ++ci) {
           const int lq = fp.chunk_logq[ci];
@@ -741,7 +750,8 @@ int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
             a.L2 = 1 << g->logN2;
             a.vranges = d_ch + ci;
             CU(launch_far_pass1(a, g->logN2, n_units, st));
-            CU(launch_far_pass2(a, g->logN1, st));
+            CU(launch_far_pass2(a, g->logN1, n_units, st));
+            CU(launch_far_reduce(a, n_units, st));
           } else {
             int l1, l2;
             split_q(lq, &l1, &l2);

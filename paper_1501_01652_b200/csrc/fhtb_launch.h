@@ -65,7 +65,10 @@ struct FarArgs {
   const double2* qlo;           // four-step twiddles e^{2 pi i m / Q}, m = hi*4096 + lo
   const double2* qhi;
   int qbits;                    // number of lo bits (<= 12)
+  const double2* cs_tab;        // (cos, sin)(-gamma k pi / L) for k = 1..L (null if gamma == 0)
 };
+
+extern int g_far_variant;       // tuning knob for the hot far-field sizes
 
 cudaError_t launch_near(const NearArgs& a, int n_tiles, int n_groups, cudaStream_t st);
 cudaError_t launch_near_reduce(const NearRowTile* rt, int n_rt, const double* part, double* F,
@@ -73,9 +76,11 @@ cudaError_t launch_near_reduce(const NearRowTile* rt, int n_rt, const double* pa
 constexpr int kNearRT = 64;
 
 // direct mode (2L power of two, unit-stride rows)
-cudaError_t launch_far_onepass(const FarArgs& a, int logN1, int n_ranges, cudaStream_t st);
+cudaError_t launch_far_onepass(const FarArgs& a, int logN1, int n_units, cudaStream_t st);
 cudaError_t launch_far_pass1(const FarArgs& a, int logN2, int n_units, cudaStream_t st);
-cudaError_t launch_far_pass2(const FarArgs& a, int logN1, cudaStream_t st);
+cudaError_t launch_far_pass2(const FarArgs& a, int logN1, int n_units, cudaStream_t st);
+cudaError_t launch_far_reduce(const FarArgs& a, int n_units, cudaStream_t st);
+cudaError_t launch_cs_table(double2* cs, long long L, double gamma, double pi_over_L, cudaStream_t st);
 
 // chirp mode (any grid length, strided output rows)
 cudaError_t launch_chirp_pass1(const FarArgs& a, int logN2, int n_units, cudaStream_t st);
