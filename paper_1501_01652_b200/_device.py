@@ -67,6 +67,8 @@ def to_dev_f64(x, dev=None):
     if isinstance(x, torch.Tensor):
         return x.to(device=dev, dtype=torch.float64).contiguous()
     a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    if not a.flags.writeable:
+        a = a.copy()
     return torch.from_numpy(a).to(dev, non_blocking=False)
 
 
