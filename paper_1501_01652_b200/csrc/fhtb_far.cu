@@ -109,6 +109,56 @@ far_pass1_kernel(FarArgs a) {
   }
 }
 
+// Pass 1, one CTA per (column group, unit, pair p): no per-element state is
+// carried across pairs, so registers hold only the FFT data.  The column
+// weights come from the grid tables W0[n-1] = omega_n^{-1/2}, IW[n-1] =
+// 1/omega_n (L2 resident) and omega_n^{-2p} = IW^{2p} by binary powering.
+template <int N2, int E, int W, int MINB>
+__global__ void __launch_bounds__(W * (N2 / E), MINB)
+far_pass1p_kernel(FarArgs a) {
+  constexpr int T = N2 / E;
+  constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
+  constexpr int NP = N2 + PAD;
+  extern __shared__ double2 sm2[];
+  const int tid = threadIdx.x, w = tid % W, tt = tid / W;
+  const int L1 = a.L1;
+  const long long n1 = (long long)blockIdx.x * W + w;
+  const int ul = blockIdx.y / a.M, p = blockIdx.y % a.M;
+  const UnitDesc U = a.units[a.u0 + ul];
+  const ReqDesc& R = a.reqs[U.req];
+  const BlockDesc& B = a.blocks[U.block];
+  long long cA, cB;
+  unit_cols(a, R, B, cA, cB);
+  double2 z[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const long long n = n1 + (long long)L1 * (tt + T * e);
+    z[e] = make_double2(0.0, 0.0);
+    if (n >= cA && n < cB) {
+      double x = a.C[(long long)R.vec * a.ldc + (n - 1)];
+      if (R.preA) x *= ipow_f(R.preA[n - 1], R.pa);
+      if (R.preB) x *= ipow_f(R.preB[n - 1], R.pb);
+      const double iw = __ldg(a.iw_tab + (n - 1));
+      double v = x * __ldg(a.w0_tab + (n - 1));
+      // v *= iw^(2p), binary powering
+      double b2 = iw * iw;
+      for (int q = p; q; q >>= 1) {
+        if (q & 1) v *= b2;
+        b2 *= b2;
+      }
+      z[e] = make_double2(v, v * iw);
+    }
+  }
+  double2* sm = sm2 + w * NP;
+  block_fft<N2, E, 1>(z, sm, tt, a.tw + (N2 - 2));
+  double2* G = a.G + ((long long)(ul * a.M + p) * N2) * L1;
+#pragma unroll
+  for (int s = 0; s < E; ++s) {
+    const int k2 = fft_out_index<N2, E>(tt, s);
+    G[(long long)k2 * L1 + n1] = cmul(z[s], qtw(a, n1 * k2));
+  }
+}
+
 // --------------------------------------------- pass 2 / one-pass epilogue
 //
 // ONEPASS: L2 == 1, N1 == 2L, one column, input generated from c.
@@ -223,6 +273,130 @@ far_pass2_kernel(FarArgs a) {
     if (kq[q]) part[kq[q] - 1] = acc[q];
 }
 
+// ------------------------------------------------- pass 2, paired-lane form
+//
+// CTA = (column pair {c, L2-c}, unit); lane pairs (2 tt, 2 tt + 1) hold the
+// same FFT index k1 of the two columns.  Half 1 transforms
+//     h[n1] = conj(G[L2-c][n1]) * e^{2 pi i n1 / L1}     (c != 0; no twiddle for c == 0)
+// so that its output V[k1] = conj(Z[2L - (c + L2 k1)]) lands on the same k1
+// as U[k1] = Z[c + L2 k1]: the DCT/DST separation of every output row needs
+// only one register exchange between the two lanes (no shared-memory round
+// trip, no barrier).  Rows c + L2 k1 (k1 < L1/2) are produced by half 0,
+// rows (L2-c) + L2 (L1-1-k1) (k1 >= L1/2) by half 1.  The gamma rotation
+// (cos th_k, sin th_k) is independent of the term index and is applied once
+// at the end (two accumulators).
+template <int N1, int E, int MINB>
+__global__ void __launch_bounds__(2 * (N1 / E), MINB)
+far_pass2x_kernel(FarArgs a) {
+  constexpr int T = N1 / E;
+  constexpr int NQ = E / 2;
+  constexpr int NP = N1 + 4;
+  using Sh = FftShape<N1, E>;
+  constexpr int RL = Sh::RL;
+  extern __shared__ double2 sm2[];
+  const int tid = threadIdx.x, h = tid & 1, tt = tid >> 1;
+  const int L = (int)a.L;
+  const int L2 = a.L2;
+  const int c = blockIdx.x;
+  const int k2b = (L2 - c) % L2;
+  const int ul = blockIdx.y;
+  const UnitDesc U = a.units[a.u0 + ul];
+  const ReqDesc& R = a.reqs[U.req];
+  const BlockDesc& B = a.blocks[U.block];
+  const double2* tw = a.tw + (N1 - 2);
+
+  // computing slots: e' = slot index in "t + T e'" order; half 0 owns
+  // e' < E/2 (k1 < L1/2), half 1 owns e' >= E/2.
+  int kq[NQ];
+  double accC[NQ], accS[NQ], rp[NQ], ir[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int e = h ? q + NQ : q;
+    const int k1 = tt + T * e;
+    int k = 0;
+    if (h == 0) {
+      k = c + L2 * k1;
+    } else if (c == 0) {
+      k = (k1 == N1 / 2) ? L : 0;
+    } else if (2 * c != L2) {
+      k = k2b + L2 * (N1 - 1 - k1);
+    }
+    if (k < 1 || k > L || k < B.r0 || k >= B.r1) k = 0;
+    kq[q] = k;
+    accC[q] = accS[q] = rp[q] = ir[q] = 0.0;
+    if (k) {
+      const double irk = a.Ld / (double)k;
+      double post = 1.0;
+      if (R.pr) post = ipow_f((double)k / a.Ld, R.pr);
+      if (R.post_e && R.pe) post *= ipow_f(R.post_e[k - 1], R.pe);
+      ir[q] = irk;
+      rp[q] = post * sqrt(irk);
+    }
+  }
+  const int mycol = h ? k2b : c;
+  for (int p = 0; p < a.M; ++p) {
+    const double2* G = a.G + ((long long)(ul * a.M + p) * L2 + mycol) * N1;
+    double2 z[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int n1 = tt + T * e;
+      double2 g = G[n1];
+      if (h) {
+        g = cconj(g);
+        if (c != 0) g = cmul(g, __ldg(tw + n1));
+      }
+      z[e] = g;
+    }
+    __syncthreads();
+    block_fft<N1, E, 1>(z, sm2 + h * NP, tt, tw);
+    // slot s holds index tt + T e, e = s/RL + (s%RL)*NB  <=>  s = (e%NB)*RL + e/NB
+    constexpr int NB = E / RL;
+    double2 own[NQ], oth[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const double2 lo = z[(q % NB) * RL + q / NB];                  // e = q
+      const double2 hi = z[((q + NQ) % NB) * RL + (q + NQ) / NB];    // e = q + NQ
+      own[q] = h ? hi : lo;
+      // partner computes the other half: send it my value at its slot
+      const double2 v = h ? lo : hi;
+      oth[q].x = __shfl_xor_sync(0xffffffffu, v.x, 1);
+      oth[q].y = __shfl_xor_sync(0xffffffffu, v.y, 1);
+    }
+    const int i0 = 2 * p, i1 = 2 * p + 1;
+    const double ac0 = R.ac[i0], as0 = R.as[i0], bc0 = R.bc[i0], bs0 = R.bs[i0];
+    const double ac1 = R.ac[i1], as1 = R.as[i1], bc1 = R.bc[i1], bs1 = R.bs[i1];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int k = kq[q];
+      if (!k) continue;
+      // Zk and conj(Z[2L-k]) of output row k
+      double2 Zk, Zp;
+      if (h == 0) { Zk = own[q]; Zp = oth[q]; }
+      else if (c == 0) { Zk = oth[q]; Zp = own[q]; }          // row L
+      else { Zk = cconj(own[q]); Zp = cconj(oth[q]); }
+      double2 Ya = make_double2(0.5 * (Zk.x + Zp.x), 0.5 * (Zk.y + Zp.y));
+      double2 Yb = make_double2(0.5 * (Zk.y - Zp.y), -0.5 * (Zk.x - Zp.x));
+      if (k == L) { Ya.y = 0.0; Yb.y = 0.0; }      // S u has no row N (schlomilch.py:314-316)
+      const double r0 = rp[q], r1 = r0 * ir[q];
+      accC[q] += r0 * (ac0 * Ya.x + bc0 * Ya.y) + r1 * (ac1 * Yb.x + bc1 * Yb.y);
+      accS[q] += r0 * (as0 * Ya.x + bs0 * Ya.y) + r1 * (as1 * Yb.x + bs1 * Yb.y);
+      rp[q] = r1 * ir[q];
+    }
+  }
+  double* part = a.part + (long long)ul * a.part_stride;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int k = kq[q];
+    if (!k) continue;
+    double v = accC[q];
+    if (a.cs_tab) {
+      const double2 th = __ldg(a.cs_tab + (k - 1));
+      v = accC[q] * th.x + accS[q] * th.y;
+    }
+    part[k - 1] = v;
+  }
+}
+
 // F[vec][j] += sum over the chunk's units of vec whose block holds row j,
 // in unit order.  Units of one vector are contiguous in the chunk.
 __global__ void far_reduce_kernel(FarArgs a, int n_units) {
@@ -247,7 +421,10 @@ __global__ void far_reduce_kernel(FarArgs a, int n_units) {
 }
 
 // ---------------------------------------------------------------- launch
-int g_far_variant = 0;
+// bits 0-3: pass-1 shape at 1024; 4-7: pass-2 shape at 2048; 8-11: paired-lane
+// pass 2; 12-15: per-pair pass 1.  Default = best measured on B200 (sweeps in
+// profiles/round1_far_variants.md).
+int g_far_variant = 16;
 
 template <int N2, int E, int W, int MINB>
 static cudaError_t p1_t(const FarArgs& a, int n_units, cudaStream_t st) {
@@ -286,7 +463,43 @@ static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
   return p2_t<N1, E, ONE, 1>(a, gx, gy, st);
 }
 
+template <int N2, int E, int W, int MINB>
+static cudaError_t p1p_t(const FarArgs& a, int n_units, cudaStream_t st) {
+  constexpr int T = N2 / E;
+  constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
+  const int smem = W * (N2 + PAD) * 16;
+  auto k = far_pass1p_kernel<N2, E, W, MINB>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  note_launch(), k<<<dim3(a.L1 / W, n_units * a.M), W * T, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int N2>
+static cudaError_t p1p_d(const FarArgs& a, int n_units, cudaStream_t st) {
+  constexpr int E = N2 >= 16 ? 16 : N2;
+  switch ((g_far_variant >> 12) & 15) {
+    case 2: return p1p_t<N2, E, (N2 >= 2048 ? 1 : 2048 / N2), 1>(a, n_units, st);
+    case 3: return p1p_t<N2, E, (N2 >= 1024 ? 1 : 1024 / N2), 2>(a, n_units, st);
+    case 4: return p1p_t<N2, E, (N2 >= 4096 ? 1 : 4096 / N2), 1>(a, n_units, st);
+    default: return p1p_t<N2, E, (N2 >= 2048 ? 1 : 2048 / N2), 2>(a, n_units, st);
+  }
+}
+
 cudaError_t launch_far_pass1(const FarArgs& a, int logN2, int n_units, cudaStream_t st) {
+  if (((g_far_variant >> 12) & 15) && a.w0_tab) {
+    switch (logN2) {
+      case 6: return p1p_d<64>(a, n_units, st);
+      case 7: return p1p_d<128>(a, n_units, st);
+      case 8: return p1p_d<256>(a, n_units, st);
+      case 9: return p1p_d<512>(a, n_units, st);
+      case 10: return p1p_d<1024>(a, n_units, st);
+      case 11: return p1p_d<2048>(a, n_units, st);
+      case 12: return p1p_d<4096>(a, n_units, st);
+      case 13: return p1p_d<8192>(a, n_units, st);
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (logN2) {
     case 6: return p1_d<64>(a, n_units, st);
     case 7: return p1_d<128>(a, n_units, st);
@@ -306,8 +519,40 @@ cudaError_t launch_far_pass1(const FarArgs& a, int logN2, int n_units, cudaStrea
   return cudaErrorInvalidValue;
 }
 
+template <int N1, int E, int MINB>
+static cudaError_t p2x_t(const FarArgs& a, int gx, int gy, cudaStream_t st) {
+  constexpr int T = N1 / E;
+  const int smem = 2 * (N1 + 4) * 16;
+  auto k = far_pass2x_kernel<N1, E, MINB>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  note_launch(), k<<<dim3(gx, gy), 2 * T, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int N1>
+static cudaError_t p2x_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
+  switch ((g_far_variant >> 8) & 15) {
+    case 2: return p2x_t<N1, 16, 2>(a, gx, gy, st);
+    case 3: return p2x_t<N1, 8, 1>(a, gx, gy, st);
+    case 4: return p2x_t<N1, 8, 2>(a, gx, gy, st);
+    default: return p2x_t<N1, 16, 1>(a, gx, gy, st);
+  }
+}
+
 cudaError_t launch_far_pass2(const FarArgs& a, int logN1, int n_units, cudaStream_t st) {
   const int gx = a.L2 / 2 + 1;
+  if ((g_far_variant >> 8) & 15) {
+    switch (logN1) {
+      case 7: return p2x_d<128>(a, gx, n_units, st);
+      case 8: return p2x_d<256>(a, gx, n_units, st);
+      case 9: return p2x_d<512>(a, gx, n_units, st);
+      case 10: return p2x_d<1024>(a, gx, n_units, st);
+      case 11: return p2x_d<2048>(a, gx, n_units, st);
+      case 12: return p2x_d<4096>(a, gx, n_units, st);
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (logN1) {
     case 7: return p2_d<128, false>(a, gx, n_units, st);
     case 8: return p2_d<256, false>(a, gx, n_units, st);
@@ -356,6 +601,21 @@ __global__ void cs_table_kernel(double2* cs, long long L, double gamma, double p
     sincos(-gamma * (double)(i + 1) * pi_over_L, &s, &c);
     cs[i] = make_double2(c, s);
   }
+}
+
+__global__ void col_tables_kernel(double* w0, double* iw, long long L, double gamma) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < L; i += (long long)gridDim.x * blockDim.x) {
+    const double om = ((double)(i + 1) + gamma) * 3.141592653589793;
+    iw[i] = 1.0 / om;
+    w0[i] = 1.0 / sqrt(om);
+  }
+}
+
+cudaError_t launch_col_tables(double* w0, double* iw, long long L, double gamma, cudaStream_t st) {
+  long long b = (L + 255) / 256;
+  if (b > 148 * 64) b = 148 * 64;
+  note_launch(), col_tables_kernel<<<(unsigned)b, 256, 0, st>>>(w0, iw, L, gamma);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_cs_table(double2* cs, long long L, double gamma, double pi_over_L, cudaStream_t st) {

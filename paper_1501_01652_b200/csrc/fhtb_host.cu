@@ -308,6 +308,8 @@ struct fhtb_grid {
   std::vector<double2*> H;         // chirp filter spectra per block
   BlockDesc* d_blocks = nullptr;
   double2* cs_tab = nullptr;       // (cos, sin)(-gamma k pi/L), k = 1..L, when gamma != 0
+  double* w0_tab = nullptr;        // omega_n^{-1/2} (direct two-pass mode)
+  double* iw_tab = nullptr;        // 1/omega_n
   // near field
   std::vector<NearTile> tiles;
   std::vector<NearRowTile> rts;
@@ -533,6 +535,11 @@ int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
     CU(launch_cs_table(g->cs_tab, g->L, g->gamma, M_PI / (double)g->L, 0));
   }
   if (g->direct && g->logN2 > 0) {
+    CU(cudaMalloc(&g->w0_tab, g->L * sizeof(double)));
+    CU(cudaMalloc(&g->iw_tab, g->L * sizeof(double)));
+    CU(launch_col_tables(g->w0_tab, g->iw_tab, g->L, g->gamma, 0));
+  }
+  if (g->direct && g->logN2 > 0) {
     double2 *ql, *qh;
     int qb;
     if (int r = get_qtab(ctx, g->logQ, &ql, &qh, &qb)) return r;
@@ -555,6 +562,8 @@ void fhtb_grid_destroy(fhtb_grid* g) {
   if (!g) return;
   cudaFree(g->d_blocks);
   cudaFree(g->cs_tab);
+  cudaFree(g->w0_tab);
+  cudaFree(g->iw_tab);
   for (double2* h : g->H) cudaFree(h);
   cudaFree(g->d_tiles);
   cudaFree(g->d_rts);
@@ -725,6 +734,8 @@ int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
       a.part = part;
       a.part_stride = g->n_out;
       a.cs_tab = g->cs_tab;
+      a.w0_tab = g->w0_tab;
+      a.iw_tab = g->iw_tab;
       if (g->direct && g->logN2 == 0) {
         a.L1 = 1 << g->logN1;
         a.L2 = 1;

@@ -66,7 +66,10 @@ struct FarArgs {
   const double2* qhi;
   int qbits;                    // number of lo bits (<= 12)
   const double2* cs_tab;        // (cos, sin)(-gamma k pi / L) for k = 1..L (null if gamma == 0)
+  const double* w0_tab;         // omega_n^{-1/2}, n = 1..L (direct mode)
+  const double* iw_tab;         // 1/omega_n
 };
+cudaError_t launch_col_tables(double* w0, double* iw, long long L, double gamma, cudaStream_t st);
 
 extern int g_far_variant;       // tuning knob for the hot far-field sizes
 
