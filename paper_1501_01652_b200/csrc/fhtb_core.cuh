@@ -125,6 +125,56 @@ template <int S> struct Dft<16, S> {
   }
 };
 
+// DFT of R points whose upper half is zero (a zero-padded R/2-point input):
+// X_2m = DFT_{R/2}(a)_m, X_{2m+1} = DFT_{R/2}(a_n w_R^n)_m.  Used by the
+// far-field pass 1, whose input n2 >= L2/2 lies beyond the grid (n > L).
+template <int R, int S> struct DftHalfZero {
+  static __device__ __forceinline__ void run(double2* v) { Dft<R, S>::run(v); }
+};
+
+template <int S> struct DftHalfZero<16, S> {
+  static __device__ __forceinline__ void run(double2* v) {
+    double2 e[8], o[8];
+    const double c1 = FHTB_COS_PI8, s1 = FHTB_SIN_PI8;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) e[n] = v[n];
+    o[0] = v[0];
+    o[1] = cmul(v[1], make_double2(c1, S * s1));
+    o[2] = mul_w8<S>(v[2]);
+    o[3] = cmul(v[3], make_double2(s1, S * c1));
+    o[4] = cmul_i<S>(v[4]);
+    o[5] = cmul(v[5], make_double2(-s1, S * c1));
+    o[6] = mul_w8_3<S>(v[6]);
+    o[7] = cmul(v[7], make_double2(-c1, S * s1));
+    Dft<8, S>::run(e);
+    Dft<8, S>::run(o);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      v[2 * m] = e[m];
+      v[2 * m + 1] = o[m];
+    }
+  }
+};
+
+template <int S> struct DftHalfZero<8, S> {
+  static __device__ __forceinline__ void run(double2* v) {
+    double2 e[4], o[4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) e[n] = v[n];
+    o[0] = v[0];
+    o[1] = mul_w8<S>(v[1]);
+    o[2] = cmul_i<S>(v[2]);
+    o[3] = mul_w8_3<S>(v[3]);
+    Dft<4, S>::run(e);
+    Dft<4, S>::run(o);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      v[2 * m] = e[m];
+      v[2 * m + 1] = o[m];
+    }
+  }
+};
+
 // ----------------------------------------------------- block Stockham FFT
 //
 // An N-point FFT executed by T threads, each holding E = N/T points in
@@ -234,13 +284,24 @@ __device__ __forceinline__ void stockham_mid(double2 (&v)[E], double2* sm, int t
 
 // Full FFT.  Caller guarantees that no other thread of the CTA still reads
 // `sm` from a previous use (a __syncthreads before the call).
-template <int N, int E, int S>
+// HZ: the upper half of the thread's first-pass inputs (slots e >= E/2) is
+// zero, except `extra` added to slot E/2 (a single element, 0 elsewhere).
+template <int N, int E, int S, bool HZ = false>
 __device__ __forceinline__ void block_fft(double2 (&v)[E], double2* sm, int t,
-                                          const double2* __restrict__ tw) {
+                                          const double2* __restrict__ tw,
+                                          double2 extra = make_double2(0.0, 0.0)) {
   using Sh = FftShape<N, E>;
   constexpr int LOGE = Sh::LOGE;
   // pass 0: radix E, Ns = 1, inputs already in place, no twiddles
-  Dft<E, S>::run(v);
+  if (HZ) {
+    DftHalfZero<E, S>::run(v);
+    if (extra.x != 0.0 || extra.y != 0.0) {
+#pragma unroll
+      for (int r = 0; r < E; ++r) v[r] = (r & 1) ? csub(v[r], extra) : cadd(v[r], extra);
+    }
+  } else {
+    Dft<E, S>::run(v);
+  }
   if (Sh::NPASS == 1) return;
 #pragma unroll
   for (int r = 0; r < E; ++r) sm[swz<LOGE>(t * E + r)] = v[r];

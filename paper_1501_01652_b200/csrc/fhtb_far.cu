@@ -85,26 +85,43 @@ far_pass1_kernel(FarArgs a) {
   const BlockDesc& B = a.blocks[U.block];
   long long cA, cB;
   unit_cols(a, R, B, cA, cB);
-  double v[E], iw[E];
+  // n = n1 + L1 n2 <= L  <=>  n2 < L2/2, or n2 = L2/2 with n1 = 0 (n = L):
+  // the upper half of every thread's slots is zero (2L = L1 L2), except one
+  // element carried separately.
+  constexpr int EH = E / 2;
+  double v[EH], iw[EH], vs = 0.0, iws = 0.0;
 #pragma unroll
-  for (int e = 0; e < E; ++e) load_col(a, R, cA, cB, n1 + (long long)L1 * (tt + T * e), v[e], iw[e]);
+  for (int e = 0; e < EH; ++e) load_col(a, R, cA, cB, n1 + (long long)L1 * (tt + T * e), v[e], iw[e]);
+  if (tt == 0 && n1 == 0) load_col(a, R, cA, cB, (long long)L1 * (T * EH), vs, iws);
   double2* sm = sm2 + w * NP;
   const double2* tw = a.tw + (N2 - 2);
+  // four-step twiddles e^{2 pi i n1 k2/Q} of this thread's outputs are the
+  // same for every pair: build them once into shared memory (thread-private
+  // slots, no synchronisation needed)
+  // slot-major so that a warp's accesses are unit stride (conflict free)
+  double2* qt = sm2 + W * NP + tid;
+  constexpr int NTH = W * T;
+#pragma unroll
+  for (int s = 0; s < E; ++s) qt[s * NTH] = qtw(a, n1 * fft_out_index<N2, E>(tt, s));
   for (int p = 0; p < a.M; ++p) {
     double2 z[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
+    for (int e = 0; e < EH; ++e) {
       const double im = v[e] * iw[e];
       z[e] = make_double2(v[e], im);
       v[e] = im * iw[e];
+      z[e + EH] = make_double2(0.0, 0.0);
     }
+    const double ims = vs * iws;
+    const double2 extra = make_double2(vs, ims);
+    vs = ims * iws;
     __syncthreads();
-    block_fft<N2, E, 1>(z, sm, tt, tw);
+    block_fft<N2, E, 1, true>(z, sm, tt, tw, extra);
     double2* G = a.G + ((long long)(ul * a.M + p) * N2) * L1;
 #pragma unroll
     for (int s = 0; s < E; ++s) {
       const int k2 = fft_out_index<N2, E>(tt, s);
-      G[(long long)k2 * L1 + n1] = cmul(z[s], qtw(a, n1 * k2));
+      G[(long long)k2 * L1 + n1] = cmul(z[s], qt[s * NTH]);
     }
   }
 }
@@ -161,10 +178,16 @@ far_pass1p_kernel(FarArgs a) {
 
 // --------------------------------------------- pass 2 / one-pass epilogue
 //
-// ONEPASS: L2 == 1, N1 == 2L, one column, input generated from c.
-template <int N1, int E, bool ONEPASS, int MINB>
-__global__ void __launch_bounds__((ONEPASS ? 1 : 2) * (N1 / E), MINB)
+// MODE 0: two-pass, columns read from G.
+// MODE 1: one-pass (L2 == 1, N1 == 2L): one column generated from c.
+// MODE 2: block whose columns all lie below L1 (narrow-column side block):
+//         pass 1 degenerates to G[n1][k2] = x[n1] e^{2 pi i n1 k2/Q}, so the
+//         columns are generated from c here and no intermediate exists.
+template <int N1, int E, int MODE, int MINB>
+__global__ void __launch_bounds__((MODE == 1 ? 1 : 2) * (N1 / E), MINB)
 far_pass2_kernel(FarArgs a) {
+  constexpr bool ONEPASS = (MODE == 1);
+  constexpr bool GEN = (MODE != 0);
   constexpr int T = N1 / E;
   constexpr int NCOL = ONEPASS ? 1 : 2;
   constexpr int NT = NCOL * T;
@@ -187,9 +210,10 @@ far_pass2_kernel(FarArgs a) {
 
   // slot geometry and row weights rp = post(k) (L/k)^{1/2} inside the block
   int kq[NQ];
-  double acc[NQ], rp[NQ], ir[NQ];
+  double acc[NQ], accS[NQ], rp[NQ], ir[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
+    accS[q] = 0.0;
     const int o = tid + NT * q;
     const int hh = o / HALF, qq = o % HALF;
     int k = 0;
@@ -210,21 +234,52 @@ far_pass2_kernel(FarArgs a) {
       rp[q] = post * sqrt(irk);
     }
   }
-  double v[E], iw[E];
-  if (ONEPASS) {
+  // GEN loaders keep per-element state across the pairs:
+  //   MODE 1: v = x omega^{-1/2}, iw = 1/omega          (z = v (1, iw))
+  //   MODE 2: V = x omega^{-1/2} e^{2 pi i m k2/Q} (complex, the four-step
+  //           twiddle folded in once), iw; columns shifted by sh = first
+  //           nonzero column (m = n - sh), undone by the row phase
+  //           phi_k = e^{i pi k sh / L} in the epilogue.
+  double v[E], vi[MODE == 2 ? E : 1], iw[E];
+  long long sh = 0;
+  double2 phi[NQ];
+  if (GEN) {
     long long cA, cB;
     unit_cols(a, R, B, cA, cB);
+    if (MODE == 2) sh = cA;
 #pragma unroll
-    for (int e = 0; e < E; ++e) load_col(a, R, cA, cB, tt + T * e, v[e], iw[e]);
+    for (int e = 0; e < E; ++e) {
+      const long long m = tt + T * e;
+      load_col(a, R, cA, cB, m + sh, v[e], iw[e]);
+      if (MODE == 2) {
+        double2 V = make_double2(v[e], 0.0);
+        if (v[e] != 0.0 && myk2 != 0) V = cmul(V, qtw(a, m * myk2));
+        v[e] = V.x;
+        vi[MODE == 2 ? e : 0] = V.y;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    phi[q] = make_double2(1.0, 0.0);
+    if (MODE == 2 && kq[q] && sh) phi[q] = qtw(a, ((long long)kq[q] * sh) % (2 * a.L));
   }
   for (int p = 0; p < a.M; ++p) {
     double2 z[E];
-    if (ONEPASS) {
+    if (GEN) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const double im = v[e] * iw[e];
-        z[e] = make_double2(v[e], im);
-        v[e] = im * iw[e];
+        if (MODE == 2) {
+          const double vr = v[e], vim = vi[MODE == 2 ? e : 0], w = iw[e];
+          z[e] = make_double2(vr - w * vim, vim + w * vr);
+          const double w2 = w * w;
+          v[e] = vr * w2;
+          vi[MODE == 2 ? e : 0] = vim * w2;
+        } else {
+          const double im = v[e] * iw[e];
+          z[e] = make_double2(v[e], im);
+          v[e] = im * iw[e];
+        }
       }
     } else {
       const double2* G = a.G + ((long long)(ul * a.M + p) * L2 + myk2) * N1;
@@ -255,22 +310,149 @@ far_pass2_kernel(FarArgs a) {
       const double2 Zp = cconj(sm2[hp * NP + swz<LOGE>(k1p)]);
       double2 Ya = make_double2(0.5 * (Zk.x + Zp.x), 0.5 * (Zk.y + Zp.y));
       double2 Yb = make_double2(0.5 * (Zk.y - Zp.y), -0.5 * (Zk.x - Zp.x));
-      if (k == L) { Ya.y = 0.0; Yb.y = 0.0; }      // S u has no row N (schlomilch.py:314-316)
-      double A0 = ac0, B0 = bc0, A1 = ac1, B1 = bc1;
-      if (a.cs_tab) {
-        const double2 th = __ldg(a.cs_tab + (k - 1));
-        A0 = ac0 * th.x + as0 * th.y; B0 = bc0 * th.x + bs0 * th.y;
-        A1 = ac1 * th.x + as1 * th.y; B1 = bc1 * th.x + bs1 * th.y;
+      if (MODE == 2 && sh) {                         // undo the column shift
+        Ya = cmul(Ya, phi[q]);
+        Yb = cmul(Yb, phi[q]);
       }
+      if (k == L) { Ya.y = 0.0; Yb.y = 0.0; }      // S u has no row N (schlomilch.py:314-316)
+      // the gamma rotation (cos th_k, sin th_k) does not depend on the term:
+      // accumulate the cos and sin parts separately, rotate once at the end
       const double r0 = rp[q], r1 = r0 * ir[q];
-      acc[q] += r0 * (A0 * Ya.x + B0 * Ya.y) + r1 * (A1 * Yb.x + B1 * Yb.y);
+      acc[q] += r0 * (ac0 * Ya.x + bc0 * Ya.y) + r1 * (ac1 * Yb.x + bc1 * Yb.y);
+      if (a.cs_tab) accS[q] += r0 * (as0 * Ya.x + bs0 * Ya.y) + r1 * (as1 * Yb.x + bs1 * Yb.y);
       rp[q] = r1 * ir[q];
     }
   }
   double* part = a.part + (long long)ul * a.part_stride;
 #pragma unroll
-  for (int q = 0; q < NQ; ++q)
-    if (kq[q]) part[kq[q] - 1] = acc[q];
+  for (int q = 0; q < NQ; ++q) {
+    const int k = kq[q];
+    if (!k) continue;
+    double val = acc[q];
+    if (a.cs_tab) {
+      const double2 th = __ldg(a.cs_tab + (k - 1));
+      val = acc[q] * th.x + accS[q] * th.y;
+    }
+    part[k - 1] = val;
+  }
+}
+
+// Pass 2 of a block whose rows all lie below L2 (narrow-row side block): only
+// k1 = 0 (and the partner k1 = L1-1) of each column FFT is needed, i.e. two
+// weighted sums over n1 per column instead of an L1-point FFT:
+//   Z[k2]           = sum_n1 G[k2][n1]
+//   Z[2L - (L2-k2)] = sum_n1 G[k2][n1] e^{-2 pi i n1 / L1}
+// CTA = (column pair {c, L2-c}, unit); a warp per column, pairs in sequence.
+__global__ void __launch_bounds__(256)
+far_rowdot_kernel(FarArgs a, int c_lo) {
+  const int L = (int)a.L;
+  const int L1 = a.L1, L2 = a.L2;
+  const int c = c_lo + blockIdx.x;
+  const int ul = blockIdx.y;
+  const UnitDesc U = a.units[a.u0 + ul];
+  const ReqDesc& R = a.reqs[U.req];
+  const BlockDesc& B = a.blocks[U.block];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // warp 0: column c, warp 1: column L2 - c (if distinct and < L2)
+  __shared__ double2 S[2][2];
+  const int cb = (L2 - c) % L2;
+  // outputs: k = c (needs Z[c] = S0(c), conj Z[2L-c] = conj S1(cb)) and
+  //          k = cb (needs Z[cb] = S0(cb), conj Z[2L-cb] = conj S1(c))
+  const int kA = c, kB = (cb != c) ? cb : 0;
+  const bool okA = kA >= 1 && kA <= L && kA >= B.r0 && kA < B.r1;
+  const bool okB = kB >= 1 && kB <= L && kB >= B.r0 && kB < B.r1;
+  if (!okA && !okB) return;
+  double rpA = 0, irA = 0, rpB = 0, irB = 0, accA = 0, accAS = 0, accB = 0, accBS = 0;
+  if (okA) {
+    irA = a.Ld / (double)kA;
+    double post = 1.0;
+    if (R.pr) post = ipow_f((double)kA / a.Ld, R.pr);
+    if (R.post_e && R.pe) post *= ipow_f(R.post_e[kA - 1], R.pe);
+    rpA = post * sqrt(irA);
+  }
+  if (okB) {
+    irB = a.Ld / (double)kB;
+    double post = 1.0;
+    if (R.pr) post = ipow_f((double)kB / a.Ld, R.pr);
+    if (R.post_e && R.pe) post *= ipow_f(R.post_e[kB - 1], R.pe);
+    rpB = post * sqrt(irB);
+  }
+  // 8 warps: warps 0-3 sum column c, warps 4-7 column cb, each a quarter of n1
+  __shared__ double2 part_s[8][2];
+  const int side_w = wid >> 2, quarter = wid & 3;
+  const int col = side_w == 0 ? c : cb;
+  const double2* rot = a.tw + (L1 - 2);   // e^{+2 pi i n1 / L1}
+  const int qlen = (L1 + 3) / 4;
+  for (int p = 0; p < a.M; ++p) {
+    {
+      const double2* g = a.G + ((long long)(ul * a.M + p) * L2 + col) * L1;
+      double2 s0 = make_double2(0, 0), s1 = make_double2(0, 0);
+      const int lo = quarter * qlen, hi = min(L1, lo + qlen);
+      for (int n1 = lo + lane; n1 < hi; n1 += 32) {
+        const double2 v = g[n1];
+        s0 = cadd(s0, v);
+        s1 = cadd(s1, cmul(v, cconj(__ldg(rot + n1))));
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        s0.x += __shfl_xor_sync(0xffffffffu, s0.x, off);
+        s0.y += __shfl_xor_sync(0xffffffffu, s0.y, off);
+        s1.x += __shfl_xor_sync(0xffffffffu, s1.x, off);
+        s1.y += __shfl_xor_sync(0xffffffffu, s1.y, off);
+      }
+      if (lane == 0) {
+        part_s[wid][0] = s0;
+        part_s[wid][1] = s1;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+      // fixed-order combination of the four quarters
+      const int sd = threadIdx.x >> 1, which = threadIdx.x & 1;
+      double2 t = part_s[4 * sd][which];
+      t = cadd(t, part_s[4 * sd + 1][which]);
+      t = cadd(t, part_s[4 * sd + 2][which]);
+      t = cadd(t, part_s[4 * sd + 3][which]);
+      S[sd][which] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int i0 = 2 * p, i1 = 2 * p + 1;
+      for (int side = 0; side < 2; ++side) {
+        const bool ok = side == 0 ? okA : okB;
+        if (!ok) continue;
+        const int k = side == 0 ? kA : kB;
+        // column of k is c (side 0) or cb (side 1); partner sum from the other column
+        const double2 Zk = S[side][0];
+        const double2 Zp = cconj(S[side ^ (cb != c ? 1 : 0)][1]);
+        double2 Ya = make_double2(0.5 * (Zk.x + Zp.x), 0.5 * (Zk.y + Zp.y));
+        double2 Yb = make_double2(0.5 * (Zk.y - Zp.y), -0.5 * (Zk.x - Zp.x));
+        if (k == L) { Ya.y = 0.0; Yb.y = 0.0; }
+        double& rp = side == 0 ? rpA : rpB;
+        const double ir = side == 0 ? irA : irB;
+        const double r0 = rp, r1 = r0 * ir;
+        const double cC = r0 * (R.ac[i0] * Ya.x + R.bc[i0] * Ya.y) + r1 * (R.ac[i1] * Yb.x + R.bc[i1] * Yb.y);
+        const double cS = r0 * (R.as[i0] * Ya.x + R.bs[i0] * Ya.y) + r1 * (R.as[i1] * Yb.x + R.bs[i1] * Yb.y);
+        if (side == 0) { accA += cC; accAS += cS; } else { accB += cC; accBS += cS; }
+        rp = r1 * ir;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double* part = a.part + (long long)ul * a.part_stride;
+    for (int side = 0; side < 2; ++side) {
+      const bool ok = side == 0 ? okA : okB;
+      if (!ok) continue;
+      const int k = side == 0 ? kA : kB;
+      double v = side == 0 ? accA : accB;
+      if (a.cs_tab) {
+        const double2 th = __ldg(a.cs_tab + (k - 1));
+        v = v * th.x + (side == 0 ? accAS : accBS) * th.y;
+      }
+      part[k - 1] = v;
+    }
+  }
 }
 
 // ------------------------------------------------- pass 2, paired-lane form
@@ -424,13 +606,13 @@ __global__ void far_reduce_kernel(FarArgs a, int n_units) {
 // bits 0-3: pass-1 shape at 1024; 4-7: pass-2 shape at 2048; 8-11: paired-lane
 // pass 2; 12-15: per-pair pass 1.  Default = best measured on B200 (sweeps in
 // profiles/round1_far_variants.md).
-int g_far_variant = 16;
+int g_far_variant = 20;
 
 template <int N2, int E, int W, int MINB>
 static cudaError_t p1_t(const FarArgs& a, int n_units, cudaStream_t st) {
   constexpr int T = N2 / E;
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
-  const int smem = W * (N2 + PAD) * 16;
+  const int smem = (W * (N2 + PAD) + W * N2) * 16;   // FFT buffers + four-step twiddles
   auto k = far_pass1_kernel<N2, E, W, MINB>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -445,22 +627,50 @@ static cudaError_t p1_d(const FarArgs& a, int n_units, cudaStream_t st) {
   return p1_t<N2, E, W, 1>(a, n_units, st);
 }
 
-template <int N1, int E, bool ONE, int MINB>
+template <int N1, int E, int MODE, int MINB>
 static cudaError_t p2_t(const FarArgs& a, int gx, int gy, cudaStream_t st) {
   constexpr int T = N1 / E;
-  constexpr int NCOL = ONE ? 1 : 2;
+  constexpr int NCOL = MODE == 1 ? 1 : 2;
   const int smem = NCOL * (N1 + 4) * 16;
-  auto k = far_pass2_kernel<N1, E, ONE, MINB>;
+  auto k = far_pass2_kernel<N1, E, MODE, MINB>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   note_launch(), k<<<dim3(gx, gy), NCOL * T, smem, st>>>(a);
   return cudaGetLastError();
 }
 
-template <int N1, bool ONE>
+template <int N1, int MODE>
 static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
-  constexpr int E = N1 >= 16 ? 16 : N1;
-  return p2_t<N1, E, ONE, 1>(a, gx, gy, st);
+  // narrow-column blocks carry a complex state per element: 8 points/thread
+  constexpr int E = MODE == 2 ? (N1 >= 8 ? 8 : N1) : (N1 >= 16 ? 16 : N1);
+  // two columns of 2048 with E = 16: 256 threads, 2 CTAs/SM measured best
+  constexpr int MINB = (MODE == 0 && N1 == 2048) ? 2
+                       : (MODE == 2 && N1 <= 1024) ? (N1 <= 512 ? 4 : 2) : 1;
+  return p2_t<N1, E, MODE, MINB>(a, gx, gy, st);
+}
+
+cudaError_t launch_far_colgen(const FarArgs& a, int logN1, int n_units, cudaStream_t st) {
+  const int gx = a.L2 / 2 + 1;
+  switch (logN1) {
+    case 1: return p2_d<2, 2>(a, gx, n_units, st);
+    case 2: return p2_d<4, 2>(a, gx, n_units, st);
+    case 3: return p2_d<8, 2>(a, gx, n_units, st);
+    case 4: return p2_d<16, 2>(a, gx, n_units, st);
+    case 5: return p2_d<32, 2>(a, gx, n_units, st);
+    case 6: return p2_d<64, 2>(a, gx, n_units, st);
+    case 7: return p2_d<128, 2>(a, gx, n_units, st);
+    case 8: return p2_d<256, 2>(a, gx, n_units, st);
+    case 9: return p2_d<512, 2>(a, gx, n_units, st);
+    case 10: return p2_d<1024, 2>(a, gx, n_units, st);
+    case 11: return p2_d<2048, 2>(a, gx, n_units, st);
+    case 12: return p2_d<4096, 2>(a, gx, n_units, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_far_rowdot(const FarArgs& a, int n_units, cudaStream_t st) {
+  note_launch(), far_rowdot_kernel<<<dim3(a.L2 / 2 + 1, n_units), 256, 0, st>>>(a, 0);
+  return cudaGetLastError();
 }
 
 template <int N2, int E, int W, int MINB>
@@ -508,6 +718,9 @@ cudaError_t launch_far_pass1(const FarArgs& a, int logN2, int n_units, cudaStrea
     case 10:
       switch (g_far_variant & 15) {
         case 1: return p1_t<1024, 16, 2, 2>(a, n_units, st);
+        case 4: return p1_t<1024, 16, 2, 3>(a, n_units, st);
+        case 5: return p1_t<1024, 16, 1, 4>(a, n_units, st);
+        case 6: return p1_t<1024, 16, 1, 6>(a, n_units, st);
         case 2: return p1_t<1024, 8, 2, 2>(a, n_units, st);
         case 3: return p1_t<1024, 8, 4, 1>(a, n_units, st);
         default: return p1_d<1024>(a, n_units, st);
@@ -554,37 +767,37 @@ cudaError_t launch_far_pass2(const FarArgs& a, int logN1, int n_units, cudaStrea
     return cudaErrorInvalidValue;
   }
   switch (logN1) {
-    case 7: return p2_d<128, false>(a, gx, n_units, st);
-    case 8: return p2_d<256, false>(a, gx, n_units, st);
-    case 9: return p2_d<512, false>(a, gx, n_units, st);
-    case 10: return p2_d<1024, false>(a, gx, n_units, st);
-    case 11:
-      switch ((g_far_variant >> 4) & 15) {
-        case 1: return p2_t<2048, 16, false, 2>(a, gx, n_units, st);
-        case 2: return p2_t<2048, 8, false, 1>(a, gx, n_units, st);
-        case 3: return p2_t<2048, 8, false, 2>(a, gx, n_units, st);
-        default: return p2_d<2048, false>(a, gx, n_units, st);
-      }
-    case 12: return p2_d<4096, false>(a, gx, n_units, st);
+    case 1: return p2_d<2, 0>(a, gx, n_units, st);
+    case 2: return p2_d<4, 0>(a, gx, n_units, st);
+    case 3: return p2_d<8, 0>(a, gx, n_units, st);
+    case 4: return p2_d<16, 0>(a, gx, n_units, st);
+    case 5: return p2_d<32, 0>(a, gx, n_units, st);
+    case 6: return p2_d<64, 0>(a, gx, n_units, st);
+    case 7: return p2_d<128, 0>(a, gx, n_units, st);
+    case 8: return p2_d<256, 0>(a, gx, n_units, st);
+    case 9: return p2_d<512, 0>(a, gx, n_units, st);
+    case 10: return p2_d<1024, 0>(a, gx, n_units, st);
+    case 11: return p2_d<2048, 0>(a, gx, n_units, st);
+    case 12: return p2_d<4096, 0>(a, gx, n_units, st);
   }
   return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_far_onepass(const FarArgs& a, int logN1, int n_units, cudaStream_t st) {
   switch (logN1) {
-    case 1: return p2_d<2, true>(a, 1, n_units, st);
-    case 2: return p2_d<4, true>(a, 1, n_units, st);
-    case 3: return p2_d<8, true>(a, 1, n_units, st);
-    case 4: return p2_d<16, true>(a, 1, n_units, st);
-    case 5: return p2_d<32, true>(a, 1, n_units, st);
-    case 6: return p2_d<64, true>(a, 1, n_units, st);
-    case 7: return p2_d<128, true>(a, 1, n_units, st);
-    case 8: return p2_d<256, true>(a, 1, n_units, st);
-    case 9: return p2_d<512, true>(a, 1, n_units, st);
-    case 10: return p2_d<1024, true>(a, 1, n_units, st);
-    case 11: return p2_d<2048, true>(a, 1, n_units, st);
-    case 12: return p2_d<4096, true>(a, 1, n_units, st);
-    case 13: return p2_d<8192, true>(a, 1, n_units, st);
+    case 1: return p2_d<2, 1>(a, 1, n_units, st);
+    case 2: return p2_d<4, 1>(a, 1, n_units, st);
+    case 3: return p2_d<8, 1>(a, 1, n_units, st);
+    case 4: return p2_d<16, 1>(a, 1, n_units, st);
+    case 5: return p2_d<32, 1>(a, 1, n_units, st);
+    case 6: return p2_d<64, 1>(a, 1, n_units, st);
+    case 7: return p2_d<128, 1>(a, 1, n_units, st);
+    case 8: return p2_d<256, 1>(a, 1, n_units, st);
+    case 9: return p2_d<512, 1>(a, 1, n_units, st);
+    case 10: return p2_d<1024, 1>(a, 1, n_units, st);
+    case 11: return p2_d<2048, 1>(a, 1, n_units, st);
+    case 12: return p2_d<4096, 1>(a, 1, n_units, st);
+    case 13: return p2_d<8192, 1>(a, 1, n_units, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -31,6 +31,7 @@ namespace {
 thread_local std::string g_err;
 int64_t g_far_chunk_bytes = 1LL << 30;     // two-pass intermediate budget
 int64_t g_near_chunk_cols = 8192;          // near-field column chunk per tile
+int g_far_prune = 1;                       // pruned side blocks (direct two-pass)
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -363,6 +364,10 @@ int fhtb_init(void) {
 
 int fhtb_set_option(const char* key, int64_t value) {
   if (!key) return fail(FHTB_EINVAL, "null key");
+  if (!std::strcmp(key, "far_prune")) {
+    g_far_prune = (int)value;
+    return FHTB_OK;
+  }
   if (!std::strcmp(key, "far_variant")) {
     g_far_variant = (int)value;
     return FHTB_OK;
@@ -523,6 +528,23 @@ int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
         x.J = 0;
         x.Mn = 0;
       }
+    } else if (g->logN2 > 0) {
+      // pruned four-step split per block (direct two-pass mode)
+      x.dmode = 0;
+      x.dlogL1 = g->logN1;
+      const long long cend = std::min(x.c1, g->n_data_cols + 1);   // columns n < cend
+      // narrow-column blocks are shifted to their first column (fhtb_far.cu MODE 2)
+      const int lc = std::max(9, ilog2ll(std::max<long long>(cend - x.c0, 2)));
+      // L2 >= r1 so that every block row has k1 = 0; keep L2 >= 1024 (the
+      // pass-1 FFT is least efficient below that) and L1 <= 2048 (rowdot sums)
+      const int lr = std::max(std::max(g->logQ - 11, 10), ilog2ll(std::max<long long>(x.r1, 2)));
+      if (g_far_prune && lc <= 12 && lc < g->logQ) {
+        x.dmode = 1;                 // narrow columns: pass 1 degenerates
+        x.dlogL1 = lc;
+      } else if (g_far_prune && lr <= 11 && lr < g->logQ && g->logQ - lr <= 13) {
+        x.dmode = 2;                 // narrow rows: pass 2 collapses to two sums
+        x.dlogL1 = g->logQ - lr;
+      }
     }
     g->bdesc.push_back(x);
   }
@@ -588,6 +610,7 @@ struct FarPlan {
   std::vector<UnitDesc> units;                 // execution order
   std::vector<int2> chunks;                    // [u0, u1) per launch group
   std::vector<int> chunk_logq;
+  std::vector<int> chunk_key;                  // direct two-pass: dmode*64 + log2 L1
   size_t g_bytes = 0;                          // intermediate
   size_t part_bytes = 0;                       // chirp partials
 };
@@ -607,21 +630,40 @@ void plan_far(const fhtb_grid* g, const std::vector<ReqDesc>& rs, FarPlan& fp) {
       all.push_back(UnitDesc{q, b, rs[q].vec, 0});
     }
   if (g->direct) {
-    fp.units = all;
-    const long long nu = (long long)all.size();
-    // one-pass: every unit in one launch; two-pass: chunks bounded by the
-    // intermediate budget.  Partial rows: one per unit of a launch.
-    const size_t ub = g->logN2 == 0 ? 0 : unit_bytes_q(g, g->logQ);
     const size_t pb = sizeof(double) * (size_t)g->n_out;
-    const long long cu = g->logN2 == 0 ? std::max<long long>(nu, 1)
-                                       : chunk_for(ub + pb, nu);
-    for (long long u0 = 0; u0 < nu; u0 += cu) {
-      fp.chunks.push_back(make_int2((int)u0, (int)std::min(nu, u0 + cu)));
-      fp.chunk_logq.push_back(g->logQ);
+    if (g->logN2 == 0) {
+      // one-pass: every unit in one launch; one partial row per unit
+      fp.units = all;
+      const long long nu = (long long)all.size();
+      if (nu) {
+        fp.chunks.push_back(make_int2(0, (int)nu));
+        fp.chunk_logq.push_back(g->logQ);
+        fp.chunk_key.push_back(-1);
+        fp.part_bytes = pb * nu;
+      }
+      return;
     }
-    if (nu) {
-      fp.g_bytes = ub * cu;
-      fp.part_bytes = pb * cu;
+    // two-pass: group units by pruned form and split (keeping vector order
+    // inside a group), chunks bounded by the intermediate budget
+    std::vector<int> keys;
+    for (auto& u : all) keys.push_back(g->bdesc[u.block].dmode * 64 + g->bdesc[u.block].dlogL1);
+    std::vector<int> uk = keys;
+    std::sort(uk.begin(), uk.end());
+    uk.erase(std::unique(uk.begin(), uk.end()), uk.end());
+    for (int key : uk) {
+      const long long start = (long long)fp.units.size();
+      for (size_t i = 0; i < all.size(); ++i)
+        if (keys[i] == key) fp.units.push_back(all[i]);
+      const long long n = (long long)fp.units.size() - start;
+      const size_t ub = (key / 64 == 1) ? 0 : unit_bytes_q(g, g->logQ);
+      const long long cu = chunk_for(ub + pb, n);
+      for (long long u0 = 0; u0 < n; u0 += cu) {
+        fp.chunks.push_back(make_int2((int)(start + u0), (int)(start + std::min(n, u0 + cu))));
+        fp.chunk_logq.push_back(g->logQ);
+        fp.chunk_key.push_back(key);
+      }
+      fp.g_bytes = std::max(fp.g_bytes, ub * (size_t)cu);
+      fp.part_bytes = std::max(fp.part_bytes, pb * (size_t)cu);
     }
     return;
   }
@@ -757,11 +799,19 @@ int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
           a.logQ = lq;
           a.u0 = fp.chunks[ci].x;
           if (g->direct) {
-            a.L1 = 1 << g->logN1;
-            a.L2 = 1 << g->logN2;
+            const int mode = fp.chunk_key[ci] / 64, l1 = fp.chunk_key[ci] % 64, l2 = g->logQ - l1;
+            a.L1 = 1 << l1;
+            a.L2 = 1 << l2;
             a.vranges = d_ch + ci;
-            CU(launch_far_pass1(a, g->logN2, n_units, st));
-            CU(launch_far_pass2(a, g->logN1, n_units, st));
+            if (mode == 1) {
+              CU(launch_far_colgen(a, l1, n_units, st));
+            } else if (mode == 2) {
+              CU(launch_far_pass1(a, l2, n_units, st));
+              CU(launch_far_rowdot(a, n_units, st));
+            } else {
+              CU(launch_far_pass1(a, l2, n_units, st));
+              CU(launch_far_pass2(a, l1, n_units, st));
+            }
             CU(launch_far_reduce(a, n_units, st));
           } else {
             int l1, l2;

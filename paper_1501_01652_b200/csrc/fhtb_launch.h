@@ -83,6 +83,8 @@ cudaError_t launch_far_onepass(const FarArgs& a, int logN1, int n_units, cudaStr
 cudaError_t launch_far_pass1(const FarArgs& a, int logN2, int n_units, cudaStream_t st);
 cudaError_t launch_far_pass2(const FarArgs& a, int logN1, int n_units, cudaStream_t st);
 cudaError_t launch_far_reduce(const FarArgs& a, int n_units, cudaStream_t st);
+cudaError_t launch_far_colgen(const FarArgs& a, int logN1, int n_units, cudaStream_t st);
+cudaError_t launch_far_rowdot(const FarArgs& a, int n_units, cudaStream_t st);
 cudaError_t launch_cs_table(double2* cs, long long L, double gamma, double pi_over_L, cudaStream_t st);
 
 // chirp mode (any grid length, strided output rows)

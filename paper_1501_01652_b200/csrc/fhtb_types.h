@@ -38,6 +38,11 @@ struct BlockDesc {
   int logQ;                 // convolution length Q = 2^logQ
   int pad_;
   const double2* H;         // FFT_Q of the chirp filter (device)
+  // direct mode: four-step split 2L = 2^dlogL1 * 2^(logQ2L - dlogL1) and the
+  // pruned form of the block: 0 full two-pass, 1 narrow columns (no pass 1),
+  // 2 narrow rows (pass 2 = two sums per column)
+  int dmode;
+  int dlogL1;
 };
 
 // Work unit of the far field: one request on one block.
