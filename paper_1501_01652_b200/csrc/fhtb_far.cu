@@ -208,7 +208,8 @@ far_pass2_kernel(FarArgs a) {
   const BlockDesc& B = a.blocks[U.block];
   const double2* tw = a.tw + (N1 - 2);
 
-  // slot geometry and row weights rp = post(k) (L/k)^{1/2} inside the block
+  // slot geometry and row weights rp = post(k) (L/k)^{1/2} inside the block;
+  // shared-memory offsets of Z[k] and Z[2L-k] are fixed per slot
   int kq[NQ];
   double acc[NQ], accS[NQ], rp[NQ], ir[NQ];
 #pragma unroll
@@ -231,7 +232,7 @@ far_pass2_kernel(FarArgs a) {
       if (R.pr) post = ipow_f((double)k / a.Ld, R.pr);
       if (R.post_e && R.pe) post *= ipow_f(R.post_e[k - 1], R.pe);
       ir[q] = irk;
-      rp[q] = post * sqrt(irk);
+      rp[q] = 0.5 * post * sqrt(irk);      // 1/2 of the DCT/DST separation folded in
     }
   }
   // GEN loaders keep per-element state across the pairs:
@@ -300,16 +301,13 @@ far_pass2_kernel(FarArgs a) {
       const int k = kq[q];
       if (!k) continue;
       const int k2 = k & (L2 - 1);
-      const int k1 = k / L2;
-      const int hk = (k2 == k2a) ? 0 : 1;
       const int kp = 2 * L - k;
       const int k2p = kp & (L2 - 1);
-      const int k1p = kp / L2;
-      const int hp = (k2p == k2a) ? 0 : 1;
-      const double2 Zk = sm2[hk * NP + swz<LOGE>(k1)];
-      const double2 Zp = cconj(sm2[hp * NP + swz<LOGE>(k1p)]);
-      double2 Ya = make_double2(0.5 * (Zk.x + Zp.x), 0.5 * (Zk.y + Zp.y));
-      double2 Yb = make_double2(0.5 * (Zk.y - Zp.y), -0.5 * (Zk.x - Zp.x));
+      const double2 Zk = sm2[((k2 == k2a) ? 0 : NP) + swz<LOGE>(k / L2)];
+      const double2 Zp = cconj(sm2[((k2p == k2a) ? 0 : NP) + swz<LOGE>(kp / L2)]);
+      // 2 Ya, 2 Yb (the factor 1/2 is folded into rp)
+      double2 Ya = make_double2(Zk.x + Zp.x, Zk.y + Zp.y);
+      double2 Yb = make_double2(Zk.y - Zp.y, Zp.x - Zk.x);
       if (MODE == 2 && sh) {                         // undo the column shift
         Ya = cmul(Ya, phi[q]);
         Yb = cmul(Yb, phi[q]);
@@ -641,6 +639,13 @@ static cudaError_t p2_t(const FarArgs& a, int gx, int gy, cudaStream_t st) {
 
 template <int N1, int MODE>
 static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
+  if (MODE == 0 && N1 == 2048) {
+    switch ((g_far_variant >> 4) & 15) {
+      case 2: return p2_t<N1, 8, MODE, 1>(a, gx, gy, st);
+      case 3: return p2_t<N1, 16, MODE, 1>(a, gx, gy, st);
+      default: break;
+    }
+  }
   // narrow-column blocks carry a complex state per element: 8 points/thread
   constexpr int E = MODE == 2 ? (N1 >= 8 ? 8 : N1) : (N1 >= 16 ? 16 : N1);
   // two columns of 2048 with E = 16: 256 threads, 2 CTAs/SM measured best
