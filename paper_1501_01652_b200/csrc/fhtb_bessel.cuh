@@ -117,26 +117,32 @@ __device__ __forceinline__ void jn_all(int omax, double z, const JOrder* __restr
     return;
   }
   const double b = fmax((double)omax, z);
-  const int k0 = miller_start(b);
+  // start at least at OMAX so the capture phase below has static indices
+  const int k0 = max(miller_start(b), OMAX);
   const double rz = 1.0 / z;
   double up = 0.0, cur = 1e-30, nrm = 0.0;
-#pragma unroll
-  for (int o = 0; o < OMAX; ++o) out[o] = 0.0;
-  for (int k = k0; k > 0; --k) {
+  // phase 1: k = k0 .. OMAX+1 produce f_{k-1} for orders >= OMAX (no capture)
+  for (int k = k0; k > OMAX; --k) {
     const double lo = fma((2.0 * k) * rz, cur, -up);
     up = cur;
     cur = lo;
-    const int o = k - 1;
-    if (o < OMAX) {
-#pragma unroll
-      for (int q = 0; q < OMAX; ++q)
-        if (q == o) out[q] = cur;
+    if (((k - 1) & 1) == 0) nrm += 2.0 * cur;
+    if (fabs(cur) > 1e250) {
+      cur *= 1e-250; up *= 1e-250; nrm *= 1e-250;
     }
+  }
+  // phase 2: k = OMAX .. 1 produce f_{OMAX-1} .. f_0, captured with static indices
+#pragma unroll
+  for (int o = OMAX - 1; o >= 0; --o) {
+    const double lo = fma((2.0 * (o + 1)) * rz, cur, -up);
+    up = cur;
+    cur = lo;
+    out[o] = cur;
     if ((o & 1) == 0) nrm += (o == 0) ? cur : 2.0 * cur;
     if (fabs(cur) > 1e250) {
       cur *= 1e-250; up *= 1e-250; nrm *= 1e-250;
 #pragma unroll
-      for (int q = 0; q < OMAX; ++q) out[q] *= 1e-250;
+      for (int q = o; q < OMAX; ++q) out[q] *= 1e-250;
     }
   }
   const double inv = 1.0 / nrm;

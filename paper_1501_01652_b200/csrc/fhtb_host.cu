@@ -850,9 +850,11 @@ int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
     na.Ld = (double)g->L;
     na.n_orders = (int)g->orders.size();
     na.omax = 0;
+    na.orders_identity = 1;
     for (int i = 0; i < na.n_orders; ++i) {
       na.orders[i] = g->orders[i];
       na.omax = std::max(na.omax, g->orders[i]);
+      if (g->orders[i] != i) na.orders_identity = 0;
     }
     na.jtab = ctx->jtab;
     na.reqs = d_req;
@@ -943,9 +945,11 @@ int fhtb_direct_apply(const fhtb_direct_desc* d, const fhtb_request* reqs, int32
   na.colv = d->col_val;
   na.Ld = d->r_scale;
   na.n_orders = d->n_orders;
+  na.orders_identity = 1;
   for (int i = 0; i < d->n_orders; ++i) {
     na.orders[i] = d->orders[i];
     na.omax = std::max(na.omax, d->orders[i]);
+    if (d->orders[i] != i) na.orders_identity = 0;
   }
   na.jtab = ctx->jtab;
   na.reqs = d_req;

@@ -26,6 +26,7 @@ struct NearArgs {
   const double* colv;           // null: column factor (n+gamma)*scale; else colv[n-1]
   double gamma, scale, Ld;
   int n_orders, omax;
+  int orders_identity;          // universe == {0, 1, ..., n_orders-1}
   int orders[kMaxOrd];
   const JOrder* jtab;           // indexed by order
   const ReqDesc* reqs;

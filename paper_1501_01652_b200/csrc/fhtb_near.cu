@@ -83,6 +83,9 @@ near_kernel(NearArgs a) {
         const double z = rf * cf;
         if (NORD == 1) {
           vals[0] = jn(a.orders[0], z, a.jtab[a.orders[0]]);
+        } else if (a.orders_identity) {
+          // universe {0, 1, ..., n-1}: one Miller sweep of NORD orders, static indices
+          jn_all<NORD>(a.omax, z, a.jtab, vals);
         } else {
           double all[kMaxOrd];
           jn_all<kMaxOrd>(a.omax, z, a.jtab, all);
