@@ -77,7 +77,27 @@ __device__ __forceinline__ double jn_miller(int nu, double z) {
   const int k0 = miller_start(b);
   const double rz = 1.0 / z;
   double up = 0.0, cur = 1e-30, nrm = 0.0, cap = 0.0;
-  for (int k = k0; k > 0; --k) {
+  // orders above nu: two steps per trip, no capture, one overflow check
+  int k = k0;
+  if ((k - nu - 1) & 1) {
+    const double lo = fma((2.0 * k) * rz, cur, -up);
+    up = cur;
+    cur = lo;
+    if (((k - 1) & 1) == 0) nrm += 2.0 * cur;
+    --k;
+  }
+  for (; k > nu + 1; k -= 2) {
+    const double lo = fma((2.0 * k) * rz, cur, -up);
+    const double lo2 = fma((2.0 * (k - 1)) * rz, lo, -cur);
+    nrm += 2.0 * (((k - 1) & 1) == 0 ? lo : lo2);
+    up = lo;
+    cur = lo2;
+    if (fabs(cur) > 1e250) {
+      cur *= 1e-250; up *= 1e-250; nrm *= 1e-250;
+    }
+  }
+  // orders nu .. 0
+  for (; k > 0; --k) {
     const double lo = fma((2.0 * k) * rz, cur, -up);
     up = cur;
     cur = lo;
@@ -121,12 +141,24 @@ __device__ __forceinline__ void jn_all(int omax, double z, const JOrder* __restr
   const int k0 = max(miller_start(b), OMAX);
   const double rz = 1.0 / z;
   double up = 0.0, cur = 1e-30, nrm = 0.0;
-  // phase 1: k = k0 .. OMAX+1 produce f_{k-1} for orders >= OMAX (no capture)
-  for (int k = k0; k > OMAX; --k) {
+  // phase 1: k = k0 .. OMAX+1 produce f_{k-1} for orders >= OMAX (no capture);
+  // two steps per trip (one even order), overflow check once per trip (the
+  // growth of two steps stays far below the 1e58 headroom)
+  int k = k0;
+  if ((k - OMAX) & 1) {
     const double lo = fma((2.0 * k) * rz, cur, -up);
     up = cur;
     cur = lo;
     if (((k - 1) & 1) == 0) nrm += 2.0 * cur;
+    --k;
+  }
+  for (; k > OMAX; k -= 2) {
+    double lo = fma((2.0 * k) * rz, cur, -up);
+    const double lo2 = fma((2.0 * (k - 1)) * rz, lo, -cur);
+    // orders k-1 and k-2: exactly one of them is even
+    nrm += 2.0 * (((k - 1) & 1) == 0 ? lo : lo2);
+    up = lo;
+    cur = lo2;
     if (fabs(cur) > 1e250) {
       cur *= 1e-250; up *= 1e-250; nrm *= 1e-250;
     }

@@ -231,10 +231,12 @@ int pack_requests(const fhtb_request* reqs, int n_req, int M, const std::vector<
 }
 
 // Group request columns (sorted by vector) so each group holds whole vectors
-// and at most 64 request columns.
-int make_groups(const std::vector<ReqDesc>& sorted, int n_vec, std::vector<int>& q0, std::vector<int>& v0) {
+// and at most kNearMaxCols request columns; *max_cols = widest group.
+int make_groups(const std::vector<ReqDesc>& sorted, int n_vec, std::vector<int>& q0, std::vector<int>& v0,
+                int* max_cols) {
   q0.clear();
   v0.clear();
+  *max_cols = 0;
   std::vector<int> cnt(n_vec, 0);
   for (auto& r : sorted) cnt[r.vec]++;
   int q = 0, v = 0;
@@ -242,8 +244,9 @@ int make_groups(const std::vector<ReqDesc>& sorted, int n_vec, std::vector<int>&
     q0.push_back(q);
     v0.push_back(v);
     int cols = 0;
-    while (v < n_vec && cols + cnt[v] <= 64) { cols += cnt[v]; q += cnt[v]; ++v; }
-    if (cols == 0) return fail(FHTB_EINVAL, "more than 64 requests for one vector");
+    while (v < n_vec && cols + cnt[v] <= kNearMaxCols) { cols += cnt[v]; q += cnt[v]; ++v; }
+    if (cols == 0 && v < n_vec) return fail(FHTB_EINVAL, "more than 128 requests for one vector");
+    *max_cols = std::max(*max_cols, cols);
   }
   q0.push_back(q);
   v0.push_back(v);
@@ -831,7 +834,8 @@ int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
 
   if ((flags & FHTB_NEAR) && !g->tiles.empty()) {
     std::vector<int> q0, v0;
-    if (int r = make_groups(rs, n_vec, q0, v0)) return r;
+    int max_cols = 0;
+    if (int r = make_groups(rs, n_vec, q0, v0, &max_cols)) return r;
     int* d_q0 = cv.take<int>(q0.size());
     int* d_v0 = cv.take<int>(v0.size());
     double* part = g->n_slots ? cv.take<double>((size_t)g->n_slots * n_vec * kNearRT) : nullptr;
@@ -868,7 +872,7 @@ int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
     na.part = part;
     na.part_stride = (long long)n_vec * kNearRT;
     na.overwrite = 0;
-    CU(launch_near(na, (int)g->tiles.size(), (int)q0.size() - 1, st));
+    CU(launch_near(na, (int)g->tiles.size(), (int)q0.size() - 1, max_cols, st));
     CU(launch_near_reduce(g->d_rts, (int)g->rts.size(), part, F, ldf, n_vec, 0, st));
   }
   return FHTB_OK;
@@ -922,7 +926,8 @@ int fhtb_direct_apply(const fhtb_direct_desc* d, const fhtb_request* reqs, int32
   long long ns = 0;
   direct_tiles(d, tiles, rts, ns);
   std::vector<int> q0, v0;
-  if (int r = make_groups(rs, n_vec, q0, v0)) return r;
+  int max_cols = 0;
+  if (int r = make_groups(rs, n_vec, q0, v0, &max_cols)) return r;
   Carve cv{(char*)ws, ws_bytes};
   ReqDesc* d_req = cv.take<ReqDesc>(n_req);
   NearTile* d_tiles = cv.take<NearTile>(std::max<size_t>(tiles.size(), 1));
@@ -963,7 +968,7 @@ int fhtb_direct_apply(const fhtb_direct_desc* d, const fhtb_request* reqs, int32
   na.part = part;
   na.part_stride = (long long)n_vec * kNearRT;
   na.overwrite = (flags & FHTB_OVERWRITE) ? 1 : 0;
-  CU(launch_near(na, (int)tiles.size(), (int)q0.size() - 1, st));
+  CU(launch_near(na, (int)tiles.size(), (int)q0.size() - 1, max_cols, st));
   CU(launch_near_reduce(d_rts, (int)rts.size(), part, F, ldf, n_vec, na.overwrite, st));
   return FHTB_OK;
 }

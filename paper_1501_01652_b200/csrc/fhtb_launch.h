@@ -74,7 +74,8 @@ cudaError_t launch_col_tables(double* w0, double* iw, long long L, double gamma,
 
 extern int g_far_variant;       // tuning knob for the hot far-field sizes
 
-cudaError_t launch_near(const NearArgs& a, int n_tiles, int n_groups, cudaStream_t st);
+cudaError_t launch_near(const NearArgs& a, int n_tiles, int n_groups, int max_cols, cudaStream_t st);
+constexpr int kNearMaxCols = 128;   // request columns per near-field CTA (largest tile)
 cudaError_t launch_near_reduce(const NearRowTile* rt, int n_rt, const double* part, double* F,
                                long long ldf, int n_vec, int overwrite, cudaStream_t st);
 constexpr int kNearRT = 64;

@@ -27,15 +27,17 @@ namespace fhtb {
 using namespace nvcuda;
 
 constexpr int kRT = kNearRT;   // output rows per tile
-constexpr int kJT = 64;        // request columns per CTA
 constexpr int kNearThreads = 256;
 
-template <int NORD> struct NearCfg {
+// JT: request columns per CTA (64, or 128 when a vector group needs more,
+// e.g. Fourier-Bessel and DHT batches -- the Bessel tile is then generated
+// once for all of them).
+template <int NORD, int JT> struct NearCfg {
   static constexpr int NK = NORD <= 2 ? 16 : (NORD <= 4 ? 8 : 4);   // grid columns per step
   static constexpr int K = NK * NORD;                                // MMA depth per step
   static constexpr int A_ELEMS = kRT * K;
-  static constexpr int B_ELEMS = K * kJT;
-  static constexpr int C_ELEMS = kRT * kJT;
+  static constexpr int B_ELEMS = K * JT;
+  static constexpr int C_ELEMS = kRT * JT;
   static constexpr int SMEM = 8 * ((A_ELEMS + B_ELEMS) > C_ELEMS ? (A_ELEMS + B_ELEMS) : C_ELEMS);
 };
 
@@ -45,15 +47,15 @@ __device__ __forceinline__ double ipow(double x, int p) {
   return r;
 }
 
-template <int NORD>
+template <int NORD, int JT>
 __global__ void __launch_bounds__(kNearThreads)
 near_kernel(NearArgs a) {
-  using Cfg = NearCfg<NORD>;
+  using Cfg = NearCfg<NORD, JT>;
   constexpr int NK = Cfg::NK, K = Cfg::K;
   extern __shared__ double smem[];
   double* As = smem;                       // [kRT][K]
-  double* Bs = smem + Cfg::A_ELEMS;        // [K][kJT]
-  double* Cs = smem;                       // [kRT][kJT] (epilogue, aliases As/Bs)
+  double* Bs = smem + Cfg::A_ELEMS;        // [K][JT]
+  double* Cs = smem;                       // [kRT][JT] (epilogue, aliases As/Bs)
 
   const NearTile tile = a.tiles[blockIdx.x];
   const int g = blockIdx.y;
@@ -62,9 +64,9 @@ near_kernel(NearArgs a) {
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
 
-  wmma::fragment<wmma::accumulator, 8, 8, 4, double> acc[kJT / 8];
+  wmma::fragment<wmma::accumulator, 8, 8, 4, double> acc[JT / 8];
 #pragma unroll
-  for (int f = 0; f < kJT / 8; ++f) wmma::fill_fragment(acc[f], 0.0);
+  for (int f = 0; f < JT / 8; ++f) wmma::fill_fragment(acc[f], 0.0);
   const int nfrag = (nq + 7) >> 3;
 
   for (long long n0 = tile.na; n0 < tile.nb; n0 += NK) {
@@ -104,8 +106,8 @@ near_kernel(NearArgs a) {
       for (int u = 0; u < NORD; ++u) As[i * K + u * NK + q] = vals[u];
     }
     // ---- weighted coefficient tile: Bs[u*NK + q][c] = w_c[u] * x_c[n]
-    for (int e = tid; e < NK * kJT; e += kNearThreads) {
-      const int q = e / kJT, c = e % kJT;
+    for (int e = tid; e < NK * JT; e += kNearThreads) {
+      const int q = e / JT, c = e % JT;
       const long long n = n0 + q;
       double x = 0.0;
       const ReqDesc* r = nullptr;
@@ -118,7 +120,7 @@ near_kernel(NearArgs a) {
         }
       }
 #pragma unroll
-      for (int u = 0; u < NORD; ++u) Bs[(u * NK + q) * kJT + c] = r ? r->w[u] * x : 0.0;
+      for (int u = 0; u < NORD; ++u) Bs[(u * NK + q) * JT + c] = r ? r->w[u] * x : 0.0;
     }
     __syncthreads();
     // ---- DMMA: warp w owns rows [8w, 8w+8)
@@ -127,10 +129,10 @@ near_kernel(NearArgs a) {
       wmma::fragment<wmma::matrix_a, 8, 8, 4, double, wmma::row_major> fa;
       wmma::load_matrix_sync(fa, As + (warp * 8) * K + kk * 4, K);
 #pragma unroll
-      for (int f = 0; f < kJT / 8; ++f) {
+      for (int f = 0; f < JT / 8; ++f) {
         if (f < nfrag) {
           wmma::fragment<wmma::matrix_b, 8, 8, 4, double, wmma::row_major> fb;
-          wmma::load_matrix_sync(fb, Bs + (kk * 4) * kJT + f * 8, kJT);
+          wmma::load_matrix_sync(fb, Bs + (kk * 4) * JT + f * 8, JT);
           wmma::mma_sync(acc[f], fa, fb, acc[f]);
         }
       }
@@ -139,8 +141,8 @@ near_kernel(NearArgs a) {
   }
   // ---- epilogue: reduce request columns into vectors with post factors
 #pragma unroll
-  for (int f = 0; f < kJT / 8; ++f)
-    wmma::store_matrix_sync(Cs + (warp * 8) * kJT + f * 8, acc[f], kJT, wmma::mem_row_major);
+  for (int f = 0; f < JT / 8; ++f)
+    wmma::store_matrix_sync(Cs + (warp * 8) * JT + f * 8, acc[f], JT, wmma::mem_row_major);
   __syncthreads();
   const int v0 = a.grp_v0[g], v1 = a.grp_v0[g + 1];
   const int nv = v1 - v0;
@@ -154,7 +156,7 @@ near_kernel(NearArgs a) {
     for (int c = 0; c < nq; ++c) {
       const ReqDesc* r = a.reqs + q0 + c;
       if (r->vec != vec) continue;
-      double p = Cs[i * kJT + c];
+      double p = Cs[i * JT + c];
       if (r->pr) p *= ipow((double)k / a.Ld, r->pr);
       if (r->post_e && r->pe) p *= ipow(r->post_e[j], r->pe);
       s += p;
@@ -183,22 +185,28 @@ __global__ void near_reduce_kernel(const NearRowTile* rt, const double* part, do
   }
 }
 
-template <int NORD>
+template <int NORD, int JT>
 static cudaError_t launch_near_t(const NearArgs& a, int n_tiles, int n_groups, cudaStream_t st) {
-  constexpr int smem = NearCfg<NORD>::SMEM;
-  cudaError_t e = cudaFuncSetAttribute(near_kernel<NORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  constexpr int smem = NearCfg<NORD, JT>::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(near_kernel<NORD, JT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  note_launch(), near_kernel<NORD><<<dim3(n_tiles, n_groups), kNearThreads, smem, st>>>(a);
+  note_launch(), near_kernel<NORD, JT><<<dim3(n_tiles, n_groups), kNearThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_near(const NearArgs& a, int n_tiles, int n_groups, cudaStream_t st) {
+template <int JT>
+static cudaError_t launch_near_j(const NearArgs& a, int n_tiles, int n_groups, cudaStream_t st) {
+  if (a.n_orders <= 1) return launch_near_t<1, JT>(a, n_tiles, n_groups, st);
+  if (a.n_orders <= 2) return launch_near_t<2, JT>(a, n_tiles, n_groups, st);
+  if (a.n_orders <= 4) return launch_near_t<4, JT>(a, n_tiles, n_groups, st);
+  if (a.n_orders <= 8) return launch_near_t<8, JT>(a, n_tiles, n_groups, st);
+  return launch_near_t<16, JT>(a, n_tiles, n_groups, st);
+}
+
+cudaError_t launch_near(const NearArgs& a, int n_tiles, int n_groups, int max_cols, cudaStream_t st) {
   if (n_tiles == 0 || n_groups == 0) return cudaSuccess;
-  if (a.n_orders <= 1) return launch_near_t<1>(a, n_tiles, n_groups, st);
-  if (a.n_orders <= 2) return launch_near_t<2>(a, n_tiles, n_groups, st);
-  if (a.n_orders <= 4) return launch_near_t<4>(a, n_tiles, n_groups, st);
-  if (a.n_orders <= 8) return launch_near_t<8>(a, n_tiles, n_groups, st);
-  return launch_near_t<16>(a, n_tiles, n_groups, st);
+  if (max_cols <= 64) return launch_near_j<64>(a, n_tiles, n_groups, st);
+  return launch_near_j<128>(a, n_tiles, n_groups, st);
 }
 
 cudaError_t launch_near_reduce(const NearRowTile* rt, int n_rt, const double* part, double* F,
