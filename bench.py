@@ -228,6 +228,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     assert np.array_equal(res.numpy(), out), "e2e result differs from the device-resident run"
+    del pinned, res
+    tasks = None if args.no_tasks else run_tasks(fh, dev, rank, world, max(2, min(args.steps, 5)), 2)
 
     if rank != 0:
         if world > 1:
@@ -235,9 +237,12 @@ def run_ours(args):
         return
 
     peak, peak_src = hbm_peak()
-    bpv = model_bytes(params, scheme)
-    far_bytes = bpv * batch
-    achieved = far_bytes / (far_ms / 1e3) / 1e9
+    # algorithmic bytes of the formulation actually executed (pruned side
+    # blocks need no or a partial intermediate), and the unpruned SURVEY 8(d)
+    # figure for reference
+    bpv = lib.fhtb_grid_far_model_bytes(grid.handle)
+    bpv_survey = model_bytes(params, scheme)
+    achieved = bpv * batch / (far_ms / 1e3) / 1e9
     line = {
         "metric": METRIC,
         "value": value,
@@ -256,14 +261,17 @@ def run_ours(args):
                    "P": params.partitions, "blocks": len(scheme.blocks), "near_field_entries": scheme.mask_size(),
                    "l2": "inputs 512 MiB/GPU > 126 MB L2; no flush", "parallelism": "dp%d (vector sharding)" % world},
         "phase_ms": {"far_field": far_ms, "near_field": near_ms},
-        "roofline": {"bound": "hbm", "kernel": "far-field pass pair (far_pass1 + far_pass2)",
+        "roofline": {"bound": "hbm", "kernel": "far field (pass 1 + pass 2 / column-generated pass 2 / row sums)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic_from_profile(), "model_bytes_per_vector": bpv,
+                     "survey_model_bytes_per_vector": bpv_survey,
+                     "survey_model_equivalent_gbs": bpv_survey * batch / (far_ms / 1e3) / 1e9,
                      "peak_source": peak_src},
         "e2e": {"value": batch * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(host.nbytes),
                 "d2h_bytes_per_step": int(out.nbytes)},
         "gpu_launches": int(l1 - l0),
         "clocks": clocks,
+        "tasks": tasks,
     }
     if world == 1 and not args.no_cpu:
         sec, ref = cpu_baseline_subprocess(n)
@@ -281,6 +289,84 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_tasks(fh, dev, rank, world, steps, warmup):
+    """The other BASELINE configs: FB (cfg3), DHT (cfg4) and cfg2 at the
+    looser eps, device-resident, CUDA-event timed, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    out = {}
+    st = torch.cuda.current_stream()
+    peak, _ = hbm_peak()
+
+    def timed(fn):
+        for _ in range(warmup):
+            fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a.record(st)
+        for _ in range(steps):
+            fn()
+        b.record(st)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    def rng(kind, n, b):
+        g = np.random.default_rng([SEED + 7, n, rank * 1000 + b])
+        return g.uniform(-1.0, 1.0, n) if kind == "u" else g.standard_normal(n)
+
+    from paper_1501_01652_b200.fourier_bessel import select_neumann_params
+    from paper_1501_01652_b200.schlomilch import SchlomilchEngine, _m_terms
+    # FB cfg3
+    n, B, eps = 2 ** 18, 16, 1e-12
+    roots = fh.bessel_roots_j0(n)
+    C = torch.from_numpy(np.stack([rng("u", n, b) for b in range(B)])).to(dev)
+    ms = timed(lambda: fh.fourier_bessel_eval(0, C, eps, roots=roots))
+    q = select_neumann_params(eps)
+    R = 2 * q.t_terms + q.k_terms - 2
+    eng = SchlomilchEngine(n, -0.25, eps / R, range(q.k_terms))
+    bpv = R * model_bytes(eng.params, eng.scheme)
+    out["fb_cfg3"] = {"config": "Fourier-Bessel order 0, N=2^18, 16 vectors U[-1,1], eps=1e-12",
+                      "transforms_per_s": B * world / (ms / 1e3), "ms_per_step": ms,
+                      "model_bytes_per_vector": bpv,
+                      "model_frac_of_hbm": bpv * B / (ms / 1e3) / 1e9 / peak}
+    # DHT cfg4
+    n, B, eps = 2 ** 16, 8, 1e-15
+    plan = fh.dht_plan(n, eps)
+    C = torch.from_numpy(np.stack([rng("n", n, b) for b in range(B)])).to(dev)
+    st_ = {}
+    fh.dht(plan, C[:1], stats=st_)
+    ms = timed(lambda: fh.dht(plan, C))
+    from paper_1501_01652_b200.dht import _shared
+    eng = _shared(plan)["engine"]
+    reqs = st_.get("schlomilch_evaluations", 0)
+    T = 2 * eng.params.m_terms * len(eng.scheme.blocks)
+    L2 = 1 << int(math.ceil(math.log2(2 * n - 1)))
+    bpv = reqs * (T * 2 * 32 * L2 + len(eng.scheme.blocks) * 8 * n + 8 * n)
+    out["dht_cfg4"] = {"config": "DHT order 0, N=2^16, 8 vectors N(0,1), eps=1e-15",
+                       "transforms_per_s": B * world / (ms / 1e3), "ms_per_step": ms,
+                       "requests_per_vector": reqs, "model": "row-restricted chirp-z (SURVEY 8(d))",
+                       "model_bytes_per_vector": bpv,
+                       "model_frac_of_hbm": bpv * B / (ms / 1e3) / 1e9 / peak}
+    # cfg2 at the looser eps
+    n, B = 2 ** 20, 64
+    Cs = torch.from_numpy(make_inputs(n, B, rank)).to(dev)
+    for eps in (1e-3, 1e-8):
+        p = fh.select_params(NU, n, eps, gamma=GAMMA)
+        ms = timed(lambda: fh.schlomilch_fast(p, Cs))
+        bpv = model_bytes(p, fh.build_partition(p))
+        out["cfg2_eps%g" % eps] = {"transforms_per_s": B * world / (ms / 1e3), "ms_per_step": ms,
+                                   "model_bytes_per_vector": bpv,
+                                   "model_frac_of_hbm": bpv * B / (ms / 1e3) / 1e9 / peak}
+    return out
 
 
 def traffic_from_profile():
@@ -363,6 +449,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline leg")
     ap.add_argument("--ref-budget", type=float, default=150.0)
     ap.add_argument("--no-e2e", action="store_true", help="device-resident timing only (profiling runs)")
+    ap.add_argument("--no-tasks", action="store_true", help="skip the FB/DHT/other-eps task timings")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

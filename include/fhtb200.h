@@ -109,6 +109,11 @@ typedef struct fhtb_request {
 
 int fhtb_grid_create(const fhtb_grid_desc* desc, fhtb_grid** out);
 void fhtb_grid_destroy(fhtb_grid* g);
+/* Algorithmic DRAM bytes of one request's far-field application in the
+ * formulation this grid executes (pruned side blocks included), following
+ * the SURVEY 8(d) byte model: intermediates written and read, coefficient
+ * reads, partial rows and output. */
+double fhtb_grid_far_model_bytes(const fhtb_grid* g);
 size_t fhtb_apply_workspace(const fhtb_grid* g, int32_t n_req, int32_t n_vec, int32_t flags);
 /* F[vec][j] += Schlomilch application of each request (far and/or near
  * field per flags).  F must be initialised by the caller (zeros for a plain

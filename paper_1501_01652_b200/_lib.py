@@ -57,6 +57,7 @@ EXPORTS = {
     "fhtb_trig_apply": (i32, [i32, i64, vp, i64, vp, vp, ctypes.c_size_t, vp]),
     "fhtb_grid_create": (i32, [ctypes.POINTER(GridDesc), ctypes.POINTER(vp)]),
     "fhtb_grid_destroy": (None, [vp]),
+    "fhtb_grid_far_model_bytes": (ctypes.c_double, [vp]),
     "fhtb_apply_workspace": (ctypes.c_size_t, [vp, i32, i32, i32]),
     "fhtb_apply": (i32, [vp, ctypes.POINTER(Request), i32, vp, i64, i32, vp, i64, i32, vp,
                          ctypes.c_size_t, vp]),

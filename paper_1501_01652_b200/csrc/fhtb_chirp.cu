@@ -135,7 +135,7 @@ chirp_pass2_kernel(FarArgs a) {
 #pragma unroll
     for (int q = 0; q < E; ++q) {
       const int k1 = fft_out_index<N1, E>(tt, q);
-      const double2 h = __ldg(H + k2 + (long long)Q2 * k1);
+      const double2 h = __ldg(H + (long long)k2 * N1 + k1);   // transposed spectrum
       y[(q / RL) + (q % RL) * (E / RL)] = cmul(z[q], h);
     }
     __syncthreads();
@@ -273,10 +273,11 @@ plain_pass1_kernel(const double2* __restrict__ in, double2* __restrict__ out, Fa
   }
 }
 
-// out[k2 + Q2 k1] = FFT_{N1}(in[k2*N1 + n1])
+// out[k2 + Q2 k1] = FFT_{N1}(in[k2*N1 + n1]); tr: out[k2*N1 + k1] (the
+// transposed spectrum layout chirp_pass2 reads row by row)
 template <int N1, int E, int S>
 __global__ void __launch_bounds__(N1 / E)
-plain_pass2_kernel(const double2* __restrict__ in, double2* __restrict__ out, FarArgs a) {
+plain_pass2_kernel(const double2* __restrict__ in, double2* __restrict__ out, FarArgs a, int tr) {
   constexpr int T = N1 / E;
   extern __shared__ double2 sm2[];
   const int tt = threadIdx.x, k2 = blockIdx.x, Q2 = a.L2;
@@ -285,7 +286,10 @@ plain_pass2_kernel(const double2* __restrict__ in, double2* __restrict__ out, Fa
   for (int e = 0; e < E; ++e) z[e] = in[(long long)k2 * N1 + tt + T * e];
   block_fft<N1, E, S>(z, sm2, tt, a.tw + (N1 - 2));
 #pragma unroll
-  for (int q = 0; q < E; ++q) out[k2 + (long long)Q2 * fft_out_index<N1, E>(tt, q)] = z[q];
+  for (int q = 0; q < E; ++q) {
+    const int k1 = fft_out_index<N1, E>(tt, q);
+    out[tr ? (long long)k2 * N1 + k1 : k2 + (long long)Q2 * k1] = z[q];
+  }
 }
 
 // h[d mod Q] = E(-s d^2) for d in [-(Mn-1), J-1], else 0
@@ -442,20 +446,20 @@ cudaError_t launch_chirp_pass2(const FarArgs& a, int logN1, int n_units, cudaStr
 }
 
 template <int N1, int S>
-static cudaError_t pp2_t(const double2* in, double2* out, const FarArgs& a, cudaStream_t st) {
+static cudaError_t pp2_t(const double2* in, double2* out, const FarArgs& a, int tr, cudaStream_t st) {
   constexpr int E = N1 >= 8 ? 8 : N1;
   const int smem = N1 * 16;
   auto k = plain_pass2_kernel<N1, E, S>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  note_launch(), k<<<dim3(a.L2), N1 / E, smem, st>>>(in, out, a);
+  note_launch(), k<<<dim3(a.L2), N1 / E, smem, st>>>(in, out, a, tr);
   return cudaGetLastError();
 }
 
 // Forward (sign -1) FFT of length Q = L1*L2 of a device vector, out-of-place
 // through `tmp`.  Used to build the chirp filter spectra.
 cudaError_t launch_plain_fft(const FarArgs& a, int logN1, int logN2, const double2* in, double2* tmp,
-                             double2* out, cudaStream_t st) {
+                             double2* out, int transposed, cudaStream_t st) {
   cudaError_t e = cudaErrorInvalidValue;
 #define PP1(N) { FHTB_W_DISPATCH_P1(N); }
 #define FHTB_W_DISPATCH_P1(N)                                                    \
@@ -478,7 +482,7 @@ cudaError_t launch_plain_fft(const FarArgs& a, int logN1, int logN2, const doubl
 #undef PP1
 #undef FHTB_W_DISPATCH_P1
   if (e != cudaSuccess) return e;
-#define PP2(N) e = pp2_t<N, -1>(tmp, out, a, st); break;
+#define PP2(N) e = pp2_t<N, -1>(tmp, out, a, transposed, st); break;
   switch (logN1) {
     case 1: PP2(2) case 2: PP2(4) case 3: PP2(8) case 4: PP2(16) case 5: PP2(32) case 6: PP2(64)
     case 7: PP2(128) case 8: PP2(256) case 9: PP2(512) case 10: PP2(1024) case 11: PP2(2048)

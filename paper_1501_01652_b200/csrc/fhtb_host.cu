@@ -330,8 +330,11 @@ void split_q(int logQ, int* l1, int* l2) {
 }
 
 // Forward FFT (sign -1) of a length-2^logQ device vector (filter spectra).
-int plain_fft(DevCtx* ctx, int logQ, const double2* in, double2* tmp, double2* out, cudaStream_t st) {
-  if (logQ <= 11) {
+// transposed: out[k2*Q1 + k1] for k = k2 + Q2*k1 under the split_q split
+// (the layout chirp_pass2 reads); else natural order.
+int plain_fft(DevCtx* ctx, int logQ, const double2* in, double2* tmp, double2* out, int transposed,
+              cudaStream_t st) {
+  if (logQ <= 11 && !transposed) {
     CU(launch_fft_batch(logQ, -1, in, out, 1, ctx->tw, st));
     return FHTB_OK;
   }
@@ -348,7 +351,7 @@ int plain_fft(DevCtx* ctx, int logQ, const double2* in, double2* tmp, double2* o
   a.qlo = ql;
   a.qhi = qh;
   a.qbits = qb;
-  CU(launch_plain_fft(a, l1, l2, in, tmp, out, st));
+  CU(launch_plain_fft(a, l1, l2, in, tmp, out, transposed, st));
   return FHTB_OK;
 }
 
@@ -521,7 +524,7 @@ int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
         CU(cudaMalloc(&tmp, Q * sizeof(double2)));
         CU(cudaMalloc(&Hb, Q * sizeof(double2)));
         CU(launch_chirp_filter(h, Q, Mn, J, g->stride, g->L, 0));
-        if (int r = plain_fft(ctx, logQ, h, tmp, Hb, 0)) return r;
+        if (int r = plain_fft(ctx, logQ, h, tmp, Hb, 1, 0)) return r;
         CU(cudaDeviceSynchronize());
         cudaFree(h);
         cudaFree(tmp);
@@ -581,6 +584,32 @@ int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
   CU(cudaDeviceSynchronize());
   *out = g;
   return FHTB_OK;
+}
+
+double fhtb_grid_far_model_bytes(const fhtb_grid* g) {
+  if (!g) return 0.0;
+  const double L = (double)g->L;
+  const int nb = (int)g->blocks.size() / 4;
+  double bytes = 8.0 * L;                                   // output row
+  for (int b = 0; b < nb; ++b) {
+    const BlockDesc& x = g->bdesc[b];
+    const double rows = (double)std::max<long long>(0, x.r1 - x.r0);
+    const double cols = (double)std::max<long long>(0, std::min(x.c1, g->n_data_cols + 1) - x.c0);
+    if (rows <= 0 || cols <= 0) continue;
+    const double terms = 2.0 * g->M;
+    bytes += 8.0 * cols + 16.0 * rows;                      // coefficients, partial row w+r
+    if (!g->direct) {                                       // chirp: two round trips of Q
+      bytes += terms * 4.0 * 16.0 * (double)(1LL << x.logQ);
+    } else if (g->logN2 == 0) {
+      // one-pass: no intermediate
+    } else if (x.dmode == 0) {
+      bytes += terms * 32.0 * L;                            // G written and read
+    } else if (x.dmode == 2) {
+      const double L2 = (double)(1LL << (g->logQ - x.dlogL1));
+      bytes += terms * 16.0 * L * (1.0 + std::min(1.0, 2.0 * (rows + 1) / L2));
+    }                                                       // dmode 1: no intermediate
+  }
+  return bytes;
 }
 
 void fhtb_grid_destroy(fhtb_grid* g) {
@@ -1018,7 +1047,7 @@ int fhtb_trig_apply(int kind, int64_t length, const double* v, int64_t batch, do
   double2* tmp = cv.take<double2>(Q);
   double2* H = cv.take<double2>(Q);
   CU(launch_chirp_filter(h, Q, length, length, 1, L, st));
-  if (int r = plain_fft(ctx, lq, h, tmp, H, st)) return r;
+  if (int r = plain_fft(ctx, lq, h, tmp, H, 0, st)) return r;
   CU(launch_trig(kind, lq, length, L, k0, k0, v, out, batch, H, ctx->tw, st));
   return FHTB_OK;
 }

@@ -97,7 +97,7 @@ cudaError_t launch_chirp_reduce(const FarArgs& a, int n_units, cudaStream_t st);
 cudaError_t launch_chirp_filter(double2* h, long long Q, long long Mn, long long J, long long s, long long L,
                                 cudaStream_t st);
 cudaError_t launch_plain_fft(const FarArgs& a, int logN1, int logN2, const double2* in, double2* tmp,
-                             double2* out, cudaStream_t st);
+                             double2* out, int transposed, cudaStream_t st);
 cudaError_t launch_trig(int kind, int logQ, long long n, long long L, long long k0, long long n0, const double* v,
                         double* out, long long batch, const double2* H, const double2* tw, cudaStream_t st);
 
