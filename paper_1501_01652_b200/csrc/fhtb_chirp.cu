@@ -25,6 +25,8 @@
 
 namespace fhtb {
 
+int g_chirp_variant = 0;   // tuning bits (performance only): 1 = pass 3 unbounded regs, 2 = pass 1 unbounded
+
 __device__ __forceinline__ double ipow_c(double x, int p) {
   double r = 1.0;
   for (int i = 0; i < p; ++i) r *= x;
@@ -48,8 +50,8 @@ __device__ __forceinline__ double2 qtw_s(const FarArgs& a, long long m, int sign
 }
 
 // ------------------------------------------------------------------ pass 1
-template <int N2, int E, int W>
-__global__ void __launch_bounds__(W * (N2 / E))
+template <int N2, int E, int W, int MINB>
+__global__ void __launch_bounds__(W * (N2 / E), MINB)
 chirp_pass1_kernel(FarArgs a) {
   constexpr int T = N2 / E;
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
@@ -107,43 +109,55 @@ chirp_pass1_kernel(FarArgs a) {
 }
 
 // ------------------------------------------------------------------ pass 2
-template <int N1, int E>
-__global__ void __launch_bounds__(N1 / E)
+// One CTA per (row k2, unit).  The filter row H_t[k2][.] and the four-step
+// twiddles e^{2 pi i n1 k2/Q} are the same for all 2M terms of the unit:
+// staged once in shared memory.  The next term's row is loaded while the
+// current one is transformed (the kernel is otherwise latency bound).
+template <int N1, int E, int MINB>
+__global__ void __launch_bounds__(N1 / E, MINB)
 chirp_pass2_kernel(FarArgs a) {
   constexpr int T = N1 / E;
   using Sh = FftShape<N1, E>;
   constexpr int RL = Sh::RL;
   extern __shared__ double2 sm2[];
+  double2* shH = sm2 + N1;
+  double2* shT = sm2 + 2 * N1;
   const int tt = threadIdx.x;
   const int k2 = blockIdx.x;
   const int ul = blockIdx.y;
-  const int Q2 = a.L2;
-  const long long Q = (long long)N1 * Q2;
+  const long long Q = (long long)N1 * a.L2;
   const UnitDesc U = a.units[a.u0 + ul];
   const BlockDesc& B = a.blocks[U.block];
-  const double2* __restrict__ H = B.H;
+  const double2* __restrict__ H = B.H + (long long)k2 * N1;   // transposed spectrum row
+  for (int x = tt; x < N1; x += T) {
+    shH[x] = __ldg(H + x);
+    shT[x] = qtw_s(a, (long long)x * k2, 1);
+  }
   const double2* tw = a.tw + (N1 - 2);
   const int nterm = 2 * a.M;
-  for (int i = 0; i < nterm; ++i) {
-    double2* row = a.G + (long long)(ul * nterm + i) * Q + (long long)k2 * N1;
+  double2* row = a.G + (long long)(ul * nterm) * Q + (long long)k2 * N1;
+  double2 zn[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) zn[e] = row[tt + T * e];
+  for (int i = 0; i < nterm; ++i, row += Q) {
     double2 z[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) z[e] = row[tt + T * e];
+    for (int e = 0; e < E; ++e) z[e] = zn[e];
+    if (i + 1 < nterm) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) zn[e] = row[Q + tt + T * e];
+    }
     __syncthreads();
     block_fft<N1, E, -1>(z, sm2, tt, tw);
     double2 y[E];
 #pragma unroll
-    for (int q = 0; q < E; ++q) {
-      const int k1 = fft_out_index<N1, E>(tt, q);
-      const double2 h = __ldg(H + (long long)k2 * N1 + k1);   // transposed spectrum
-      y[(q / RL) + (q % RL) * (E / RL)] = cmul(z[q], h);
-    }
+    for (int q = 0; q < E; ++q) y[(q / RL) + (q % RL) * (E / RL)] = cmul(z[q], shH[fft_out_index<N1, E>(tt, q)]);
     __syncthreads();
     block_fft<N1, E, 1>(y, sm2, tt, tw);
 #pragma unroll
     for (int q = 0; q < E; ++q) {
       const int n1 = fft_out_index<N1, E>(tt, q);
-      row[n1] = cmul(y[q], qtw_s(a, (long long)n1 * k2, 1));
+      row[n1] = cmul(y[q], shT[n1]);
     }
   }
 }
@@ -152,8 +166,17 @@ chirp_pass2_kernel(FarArgs a) {
 // One CTA per (column group, unit): all 2M terms of the unit are reduced in
 // registers and written as a per-unit partial row part[unit][j]; the
 // partials of one vector are summed in unit order by chirp_reduce_kernel.
-template <int N2, int E, int W>
-__global__ void __launch_bounds__(W * (N2 / E))
+//
+// Row j (k = k0 + s j) of term i contributes
+//   rp0 (L/k)^i [cos(th) Re((a_i - i b_i) w_i) + sin(th) Re((as_i - i bs_i) w_i)]
+// with w_i = Y_i * oc (oc = out-chirp / Q) and th = -gamma pi k/L.  The
+// per-term scalars satisfy as_i = -b_i, bs_i = a_i (pack_requests), so the
+// second sum is Im of the first: one complex accumulator S, folded by
+// Horner's rule in 1/k from the last term down, S <- S (L/k) + (a_i - i b_i) Y_i;
+// oc, rp0 and the rotation are applied once at the end.  The next term's
+// column is loaded while the current one is transformed.
+template <int N2, int E, int W, int MINB>
+__global__ void __launch_bounds__(W * (N2 / E), MINB)
 chirp_pass3_kernel(FarArgs a) {
   constexpr int T = N2 / E;
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
@@ -165,66 +188,66 @@ chirp_pass3_kernel(FarArgs a) {
   const long long n1 = (long long)blockIdx.x * W + w;
   const int ul = blockIdx.y;
   const long long L = a.L, k0 = a.first, s = a.stride;
-  const double invQ = 1.0 / (double)Q;
   const UnitDesc U = a.units[a.u0 + ul];
   const ReqDesc& R = a.reqs[U.req];
   const BlockDesc& B = a.blocks[U.block];
-  const long long n0 = B.c0;
-  double acc[E], rp[E], ir[E];
-  double2 oc[E];
+  double ir[E];
+  double2 SC[E];
 #pragma unroll
   for (int q = 0; q < E; ++q) {
     const long long j = n1 + (long long)Q1 * fft_out_index<N2, E>(tt, q);
     const long long k = k0 + s * j;
-    acc[q] = rp[q] = ir[q] = 0.0;
-    oc[q] = make_double2(0.0, 0.0);
-    if (j < B.J && k >= B.r0 && k < B.r1 && k <= L) {
-      const double irk = a.Ld / (double)k;
-      double post = 1.0;
-      if (R.pr) post = ipow_c((double)k / a.Ld, R.pr);
-      if (R.post_e && R.pe) post *= ipow_c(R.post_e[j], R.pe);
-      ir[q] = irk;
-      rp[q] = post * sqrt(irk);
-      const long long P = 2 * k0 * n0 + 2 * s * j * n0 + s * ((j * j) % (4 * L));
-      const double2 c = chirpE(P, L);
-      oc[q] = make_double2(c.x * invQ, c.y * invQ);
-    }
-  }
-  double thc[E], ths[E];
-#pragma unroll
-  for (int q = 0; q < E; ++q) {
-    thc[q] = 1.0;
-    ths[q] = 0.0;
-    if (a.gamma != 0.0 && rp[q] != 0.0) {
-      const long long j = n1 + (long long)Q1 * fft_out_index<N2, E>(tt, q);
-      sincos(-a.gamma * (double)(k0 + s * j) * a.pi_over_L, &ths[q], &thc[q]);
-    }
+    ir[q] = (j < B.J && k >= B.r0 && k < B.r1 && k <= L) ? a.Ld / (double)k : 0.0;
+    SC[q] = make_double2(0.0, 0.0);
   }
   double2* sm = sm2 + w * NP;
   const double2* tw = a.tw + (N2 - 2);
   const int nterm = 2 * a.M;
-  for (int i = 0; i < nterm; ++i) {
-    const double2* G = a.G + (long long)(ul * nterm + i) * Q;
+  const double2* G = a.G + (long long)(ul * nterm + nterm - 1) * Q + n1;
+  double2 zn[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) zn[e] = G[(long long)(tt + T * e) * Q1];
+  for (int i = nterm - 1; i >= 0; --i, G -= Q) {
     double2 z[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) z[e] = G[(long long)(tt + T * e) * Q1 + n1];
+    for (int e = 0; e < E; ++e) z[e] = zn[e];
+    if (i > 0) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) zn[e] = G[(long long)(tt + T * e) * Q1 - Q];
+    }
     __syncthreads();
     block_fft<N2, E, 1>(z, sm, tt, tw);
-    const double ac = R.ac[i], as_ = R.as[i], bc = R.bc[i], bs = R.bs[i];
+    const double ac = R.ac[i], bc = R.bc[i];
 #pragma unroll
     for (int q = 0; q < E; ++q) {
-      if (rp[q] == 0.0) continue;
-      const double2 Y = cmul(z[q], oc[q]);
-      const double A = ac * thc[q] + as_ * ths[q], Bv = bc * thc[q] + bs * ths[q];
-      acc[q] += rp[q] * (A * Y.x + Bv * Y.y);
-      rp[q] *= ir[q];
+      // S = S * ir + (ac - i bc) z
+      SC[q].x = fma(SC[q].x, ir[q], fma(ac, z[q].x, bc * z[q].y));
+      SC[q].y = fma(SC[q].y, ir[q], fma(ac, z[q].y, -bc * z[q].x));
     }
   }
+  const double invQ = 1.0 / (double)Q;
+  const long long n0 = B.c0;
   double* part = a.part + (long long)ul * a.part_stride;
 #pragma unroll
   for (int q = 0; q < E; ++q) {
     const long long j = n1 + (long long)Q1 * fft_out_index<N2, E>(tt, q);
-    if (j < a.n_out && ir[q] != 0.0) part[j] = acc[q];
+    if (j < a.n_out && ir[q] != 0.0) {
+      const long long k = k0 + s * j;
+      double post = 1.0;
+      if (R.pr) post = ipow_c((double)k / a.Ld, R.pr);
+      if (R.post_e && R.pe) post *= ipow_c(R.post_e[j], R.pe);
+      const double rp0 = post * sqrt(ir[q]) * invQ;
+      const long long P = 2 * k0 * n0 + 2 * s * j * n0 + s * ((j * j) % (4 * L));
+      const double2 oc = chirpE(P, L);
+      const double2 wv = cmul(oc, SC[q]);
+      double v = wv.x;
+      if (a.gamma != 0.0) {
+        double th, tc;
+        sincos(-a.gamma * (double)k * a.pi_over_L, &th, &tc);
+        v = tc * wv.x + th * wv.y;
+      }
+      part[j] = rp0 * v;
+    }
   }
 }
 
@@ -361,7 +384,8 @@ static cudaError_t c1_w(const FarArgs& a, int n_units, cudaStream_t st) {
   constexpr int E = N2 >= 8 ? 8 : N2;
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
   const int smem = W * (N2 + PAD) * 16;
-  auto k = chirp_pass1_kernel<N2, E, W>;
+  constexpr int MB = (W * (N2 / E)) >= 256 ? 2 : 1;
+  auto k = (g_chirp_variant & 2) ? chirp_pass1_kernel<N2, E, W, 1> : chirp_pass1_kernel<N2, E, W, MB>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   note_launch(), k<<<dim3(a.L1 / W, n_units), W * (N2 / E), smem, st>>>(a);
@@ -373,7 +397,8 @@ static cudaError_t c3_w(const FarArgs& a, int n_ranges, cudaStream_t st) {
   constexpr int E = N2 >= 8 ? 8 : N2;
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
   const int smem = W * (N2 + PAD) * 16;
-  auto k = chirp_pass3_kernel<N2, E, W>;
+  constexpr int MB = (W * (N2 / E)) >= 256 ? 2 : 1;
+  auto k = (g_chirp_variant & 1) ? chirp_pass3_kernel<N2, E, W, 1> : chirp_pass3_kernel<N2, E, W, MB>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   note_launch(), k<<<dim3(a.L1 / W, n_ranges), W * (N2 / E), smem, st>>>(a);
@@ -430,8 +455,9 @@ cudaError_t launch_chirp_pass3(const FarArgs& a, int logN2, int n_ranges, cudaSt
 template <int N1>
 static cudaError_t c2_t(const FarArgs& a, int n_units, cudaStream_t st) {
   constexpr int E = N1 >= 8 ? 8 : N1;
-  const int smem = N1 * 16;
-  auto k = chirp_pass2_kernel<N1, E>;
+  const int smem = 3 * N1 * 16;
+  constexpr int MB = N1 / E <= 32 ? 16 : (N1 / E <= 64 ? 8 : (N1 / E <= 128 ? 4 : 2));
+  auto k = chirp_pass2_kernel<N1, E, MB>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   note_launch(), k<<<dim3(a.L2, n_units), N1 / E, smem, st>>>(a);

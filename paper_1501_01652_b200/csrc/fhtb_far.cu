@@ -181,13 +181,23 @@ far_pass1p_kernel(FarArgs a) {
 // MODE 0: two-pass, columns read from G.
 // MODE 1: one-pass (L2 == 1, N1 == 2L): one column generated from c.
 // MODE 2: block whose columns all lie below L1 (narrow-column side block):
-//         pass 1 degenerates to G[n1][k2] = x[n1] e^{2 pi i n1 k2/Q}, so the
-//         columns are generated from c here and no intermediate exists.
+//         pass 1 degenerates to G[n1][k2] = u[n1] e^{2 pi i n1 k2/Q}, so the
+//         columns are formed here from the per-unit table u (colgen_prep)
+//         and no intermediate exists.
+//
+// Epilogue algebra.  Term i of row k adds r_i (a_i Y.x + b_i Y.y) to the
+// cosine part and r_i (as_i Y.x + bs_i Y.y) to the sine part of the gamma
+// rotation, with as_i = -b_i, bs_i = a_i (pack_requests).  Both are one
+// complex sum U = sum_i r_i (a_i - i b_i) Y_i: cosine part Re U, sine part
+// Im U.  With r_{2p} = r_0 (L/k)^{2p}, r_{2p+1} = r_{2p} L/k, U is folded by
+// Horner's rule over the pairs from the last one down (MODE 0 / 2; MODE 1
+// generates its columns by a forward recurrence and keeps r explicitly);
+// r_0 and the MODE-2 column-shift phase phi_k are applied once at the end.
 template <int N1, int E, int MODE, int MINB>
 __global__ void __launch_bounds__((MODE == 1 ? 1 : 2) * (N1 / E), MINB)
 far_pass2_kernel(FarArgs a) {
   constexpr bool ONEPASS = (MODE == 1);
-  constexpr bool GEN = (MODE != 0);
+  constexpr bool HOR = (MODE != 1);
   constexpr int T = N1 / E;
   constexpr int NCOL = ONEPASS ? 1 : 2;
   constexpr int NT = NCOL * T;
@@ -208,13 +218,11 @@ far_pass2_kernel(FarArgs a) {
   const BlockDesc& B = a.blocks[U.block];
   const double2* tw = a.tw + (N1 - 2);
 
-  // slot geometry and row weights rp = post(k) (L/k)^{1/2} inside the block;
-  // shared-memory offsets of Z[k] and Z[2L-k] are fixed per slot
   int kq[NQ];
-  double acc[NQ], accS[NQ], rp[NQ], ir[NQ];
+  double ir[NQ], rp[HOR ? 1 : NQ];
+  double2 acc[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
-    accS[q] = 0.0;
     const int o = tid + NT * q;
     const int hh = o / HALF, qq = o % HALF;
     int k = 0;
@@ -225,63 +233,46 @@ far_pass2_kernel(FarArgs a) {
       if (k < 1 || k > L || k < B.r0 || k >= B.r1) k = 0;
     }
     kq[q] = k;
-    acc[q] = rp[q] = ir[q] = 0.0;
-    if (k) {
-      const double irk = a.Ld / (double)k;
+    acc[q] = make_double2(0.0, 0.0);
+    ir[q] = k ? a.Ld / (double)k : 0.0;
+    if (!HOR) {
       double post = 1.0;
-      if (R.pr) post = ipow_f((double)k / a.Ld, R.pr);
-      if (R.post_e && R.pe) post *= ipow_f(R.post_e[k - 1], R.pe);
-      ir[q] = irk;
-      rp[q] = 0.5 * post * sqrt(irk);      // 1/2 of the DCT/DST separation folded in
+      if (k && R.pr) post = ipow_f((double)k / a.Ld, R.pr);
+      if (k && R.post_e && R.pe) post *= ipow_f(R.post_e[k - 1], R.pe);
+      rp[HOR ? 0 : q] = k ? 0.5 * post * sqrt(ir[q]) : 0.0;
     }
   }
-  // GEN loaders keep per-element state across the pairs:
-  //   MODE 1: v = x omega^{-1/2}, iw = 1/omega          (z = v (1, iw))
-  //   MODE 2: V = x omega^{-1/2} e^{2 pi i m k2/Q} (complex, the four-step
-  //           twiddle folded in once), iw; columns shifted by sh = first
-  //           nonzero column (m = n - sh), undone by the row phase
-  //           phi_k = e^{i pi k sh / L} in the epilogue.
-  double v[E], vi[MODE == 2 ? E : 1], iw[E];
-  long long sh = 0;
-  double2 phi[NQ];
-  if (GEN) {
+  // column sources
+  //   MODE 1: v = x omega^{-1/2}, iw = 1/omega kept per element (z = v (1, iw),
+  //           v *= iw^2 per pair)
+  //   MODE 2: tq = e^{2 pi i m k2/Q} per element; z = u_p[m] tq
+  double v[ONEPASS ? E : 1], iw[ONEPASS ? E : 1];
+  double2 tq[MODE == 2 ? E : 1];
+  if (ONEPASS) {
     long long cA, cB;
     unit_cols(a, R, B, cA, cB);
-    if (MODE == 2) sh = cA;
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const long long m = tt + T * e;
-      load_col(a, R, cA, cB, m + sh, v[e], iw[e]);
-      if (MODE == 2) {
-        double2 V = make_double2(v[e], 0.0);
-        if (v[e] != 0.0 && myk2 != 0) V = cmul(V, qtw(a, m * myk2));
-        v[e] = V.x;
-        vi[MODE == 2 ? e : 0] = V.y;
-      }
-    }
+    for (int e = 0; e < E; ++e) load_col(a, R, cA, cB, tt + T * e, v[ONEPASS ? e : 0], iw[ONEPASS ? e : 0]);
   }
+  if (MODE == 2) {
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    phi[q] = make_double2(1.0, 0.0);
-    if (MODE == 2 && kq[q] && sh) phi[q] = qtw(a, ((long long)kq[q] * sh) % (2 * a.L));
+    for (int e = 0; e < E; ++e)
+      tq[MODE == 2 ? e : 0] = myk2 ? qtw(a, (long long)(tt + T * e) * myk2) : make_double2(1.0, 0.0);
   }
-  for (int p = 0; p < a.M; ++p) {
+  for (int pi = 0; pi < a.M; ++pi) {
+    const int p = HOR ? a.M - 1 - pi : pi;
     double2 z[E];
-    if (GEN) {
+    if (ONEPASS) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        if (MODE == 2) {
-          const double vr = v[e], vim = vi[MODE == 2 ? e : 0], w = iw[e];
-          z[e] = make_double2(vr - w * vim, vim + w * vr);
-          const double w2 = w * w;
-          v[e] = vr * w2;
-          vi[MODE == 2 ? e : 0] = vim * w2;
-        } else {
-          const double im = v[e] * iw[e];
-          z[e] = make_double2(v[e], im);
-          v[e] = im * iw[e];
-        }
+        const double im = v[ONEPASS ? e : 0] * iw[ONEPASS ? e : 0];
+        z[e] = make_double2(v[ONEPASS ? e : 0], im);
+        v[ONEPASS ? e : 0] = im * iw[ONEPASS ? e : 0];
       }
+    } else if (MODE == 2) {
+      const double2* u = a.G + (long long)(ul * a.M + p) * N1;
+#pragma unroll
+      for (int e = 0; e < E; ++e) z[e] = cmul(u[tt + T * e], tq[MODE == 2 ? e : 0]);
     } else {
       const double2* G = a.G + ((long long)(ul * a.M + p) * L2 + myk2) * N1;
 #pragma unroll
@@ -294,44 +285,89 @@ far_pass2_kernel(FarArgs a) {
     for (int s = 0; s < E; ++s) sm2[h * NP + swz<LOGE>(fft_out_index<N1, E>(tt, s))] = z[s];
     __syncthreads();
     const int i0 = 2 * p, i1 = 2 * p + 1;
-    const double ac0 = R.ac[i0], as0 = R.as[i0], bc0 = R.bc[i0], bs0 = R.bs[i0];
-    const double ac1 = R.ac[i1], as1 = R.as[i1], bc1 = R.bc[i1], bs1 = R.bs[i1];
+    const double ac0 = R.ac[i0], bc0 = R.bc[i0];
+    const double ac1 = R.ac[i1], bc1 = R.bc[i1];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int k = kq[q];
       if (!k) continue;
-      const int k2 = k & (L2 - 1);
       const int kp = 2 * L - k;
-      const int k2p = kp & (L2 - 1);
-      const double2 Zk = sm2[((k2 == k2a) ? 0 : NP) + swz<LOGE>(k / L2)];
-      const double2 Zp = cconj(sm2[((k2p == k2a) ? 0 : NP) + swz<LOGE>(kp / L2)]);
-      // 2 Ya, 2 Yb (the factor 1/2 is folded into rp)
+      const double2 Zk = sm2[(((k & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(k / L2)];
+      const double2 Zp = cconj(sm2[(((kp & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(kp / L2)]);
+      // 2 Ya, 2 Yb (the factor 1/2 is folded into r_0)
       double2 Ya = make_double2(Zk.x + Zp.x, Zk.y + Zp.y);
       double2 Yb = make_double2(Zk.y - Zp.y, Zp.x - Zk.x);
-      if (MODE == 2 && sh) {                         // undo the column shift
-        Ya = cmul(Ya, phi[q]);
-        Yb = cmul(Yb, phi[q]);
-      }
       if (k == L) { Ya.y = 0.0; Yb.y = 0.0; }      // S u has no row N (schlomilch.py:314-316)
-      // the gamma rotation (cos th_k, sin th_k) does not depend on the term:
-      // accumulate the cos and sin parts separately, rotate once at the end
-      const double r0 = rp[q], r1 = r0 * ir[q];
-      acc[q] += r0 * (ac0 * Ya.x + bc0 * Ya.y) + r1 * (ac1 * Yb.x + bc1 * Yb.y);
-      if (a.cs_tab) accS[q] += r0 * (as0 * Ya.x + bs0 * Ya.y) + r1 * (as1 * Yb.x + bs1 * Yb.y);
-      rp[q] = r1 * ir[q];
+      // t0 = (a0 - i b0) Ya, t1 = (a1 - i b1) Yb
+      const double t0x = fma(ac0, Ya.x, bc0 * Ya.y), t0y = fma(ac0, Ya.y, -bc0 * Ya.x);
+      const double t1x = fma(ac1, Yb.x, bc1 * Yb.y), t1y = fma(ac1, Yb.y, -bc1 * Yb.x);
+      const double w = ir[q];
+      if (HOR) {
+        const double w2 = w * w;
+        acc[q].x = fma(acc[q].x, w2, fma(w, t1x, t0x));
+        acc[q].y = fma(acc[q].y, w2, fma(w, t1y, t0y));
+      } else {
+        const double r0 = rp[HOR ? 0 : q], r1 = r0 * w;
+        acc[q].x = fma(r0, t0x, fma(r1, t1x, acc[q].x));
+        acc[q].y = fma(r0, t0y, fma(r1, t1y, acc[q].y));
+        rp[HOR ? 0 : q] = r1 * w;
+      }
     }
+  }
+  long long sh = 0;
+  if (MODE == 2) {
+    long long cA, cB;
+    unit_cols(a, R, B, cA, cB);
+    sh = cA;
   }
   double* part = a.part + (long long)ul * a.part_stride;
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int k = kq[q];
     if (!k) continue;
-    double val = acc[q];
+    double2 u = acc[q];
+    if (HOR) {
+      double post = 1.0;
+      if (R.pr) post = ipow_f((double)k / a.Ld, R.pr);
+      if (R.post_e && R.pe) post *= ipow_f(R.post_e[k - 1], R.pe);
+      const double r0 = 0.5 * post * sqrt(ir[q]);
+      u = make_double2(u.x * r0, u.y * r0);
+    }
+    if (MODE == 2 && sh) {
+      // phi_k = e^{i pi k sh / L}; exactly (-1)^sh at k = L
+      const double2 phi = (k == L) ? make_double2((sh & 1) ? -1.0 : 1.0, 0.0)
+                                   : qtw(a, ((long long)k * sh) % (2 * a.L));
+      u = cmul(u, phi);
+    }
+    double val = u.x;
     if (a.cs_tab) {
       const double2 th = __ldg(a.cs_tab + (k - 1));
-      val = acc[q] * th.x + accS[q] * th.y;
+      val = u.x * th.x + u.y * th.y;
     }
     part[k - 1] = val;
+  }
+}
+
+// Column table of a narrow-column (MODE 2) unit, shifted to its first column
+// sh: u_p[m] = x_n omega_n^{-1/2} omega_n^{-2p} (1, 1/omega_n), n = m + sh,
+// p < M, m < L1 (terms 2p and 2p+1 as the real and imaginary part).
+__global__ void colgen_prep_kernel(FarArgs a) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ul = blockIdx.y;
+  if (m >= a.L1) return;
+  const UnitDesc U = a.units[a.u0 + ul];
+  const ReqDesc& R = a.reqs[U.req];
+  const BlockDesc& B = a.blocks[U.block];
+  long long cA, cB;
+  unit_cols(a, R, B, cA, cB);
+  const long long n = m + cA;
+  double v, iw;
+  load_col(a, R, cA, cB, n, v, iw);
+  double2* u = a.G + (long long)(ul * a.M) * a.L1 + m;
+  for (int p = 0; p < a.M; ++p) {
+    const double im = v * iw;
+    u[(long long)p * a.L1] = make_double2(v, im);
+    v = im * iw;
   }
 }
 
@@ -340,7 +376,11 @@ far_pass2_kernel(FarArgs a) {
 // weighted sums over n1 per column instead of an L1-point FFT:
 //   Z[k2]           = sum_n1 G[k2][n1]
 //   Z[2L - (L2-k2)] = sum_n1 G[k2][n1] e^{-2 pi i n1 / L1}
-// CTA = (column pair {c, L2-c}, unit); a warp per column, pairs in sequence.
+// CTA = (column pair {c, L2-c}, unit); warps 0-3 sum column c, warps 4-7
+// column L2-c, each over a quarter of n1, for all pairs first (loads of all
+// pairs in flight together), then two threads combine the quarters in fixed
+// order and run the epilogue (same algebra as far_pass2_kernel).
+constexpr int kMaxPairs = 16;
 __global__ void __launch_bounds__(256)
 far_rowdot_kernel(FarArgs a, int c_lo) {
   const int L = (int)a.L;
@@ -351,8 +391,6 @@ far_rowdot_kernel(FarArgs a, int c_lo) {
   const ReqDesc& R = a.reqs[U.req];
   const BlockDesc& B = a.blocks[U.block];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  // warp 0: column c, warp 1: column L2 - c (if distinct and < L2)
-  __shared__ double2 S[2][2];
   const int cb = (L2 - c) % L2;
   // outputs: k = c (needs Z[c] = S0(c), conj Z[2L-c] = conj S1(cb)) and
   //          k = cb (needs Z[cb] = S0(cb), conj Z[2L-cb] = conj S1(c))
@@ -360,97 +398,73 @@ far_rowdot_kernel(FarArgs a, int c_lo) {
   const bool okA = kA >= 1 && kA <= L && kA >= B.r0 && kA < B.r1;
   const bool okB = kB >= 1 && kB <= L && kB >= B.r0 && kB < B.r1;
   if (!okA && !okB) return;
-  double rpA = 0, irA = 0, rpB = 0, irB = 0, accA = 0, accAS = 0, accB = 0, accBS = 0;
-  if (okA) {
-    irA = a.Ld / (double)kA;
-    double post = 1.0;
-    if (R.pr) post = ipow_f((double)kA / a.Ld, R.pr);
-    if (R.post_e && R.pe) post *= ipow_f(R.post_e[kA - 1], R.pe);
-    rpA = post * sqrt(irA);
-  }
-  if (okB) {
-    irB = a.Ld / (double)kB;
-    double post = 1.0;
-    if (R.pr) post = ipow_f((double)kB / a.Ld, R.pr);
-    if (R.post_e && R.pe) post *= ipow_f(R.post_e[kB - 1], R.pe);
-    rpB = post * sqrt(irB);
-  }
-  // 8 warps: warps 0-3 sum column c, warps 4-7 column cb, each a quarter of n1
-  __shared__ double2 part_s[8][2];
+  __shared__ double2 part_s[8][kMaxPairs][2];
   const int side_w = wid >> 2, quarter = wid & 3;
   const int col = side_w == 0 ? c : cb;
   const double2* rot = a.tw + (L1 - 2);   // e^{+2 pi i n1 / L1}
   const int qlen = (L1 + 3) / 4;
+  const int lo = quarter * qlen, hi = min(L1, lo + qlen);
   for (int p = 0; p < a.M; ++p) {
-    {
-      const double2* g = a.G + ((long long)(ul * a.M + p) * L2 + col) * L1;
-      double2 s0 = make_double2(0, 0), s1 = make_double2(0, 0);
-      const int lo = quarter * qlen, hi = min(L1, lo + qlen);
-      for (int n1 = lo + lane; n1 < hi; n1 += 32) {
-        const double2 v = g[n1];
-        s0 = cadd(s0, v);
-        s1 = cadd(s1, cmul(v, cconj(__ldg(rot + n1))));
-      }
+    const double2* g = a.G + ((long long)(ul * a.M + p) * L2 + col) * L1;
+    double2 s0 = make_double2(0, 0), s1 = make_double2(0, 0);
+#pragma unroll 4
+    for (int n1 = lo + lane; n1 < hi; n1 += 32) {
+      const double2 v = g[n1];
+      s0 = cadd(s0, v);
+      s1 = cadd(s1, cmul(v, cconj(__ldg(rot + n1))));
+    }
 #pragma unroll
-      for (int off = 16; off; off >>= 1) {
-        s0.x += __shfl_xor_sync(0xffffffffu, s0.x, off);
-        s0.y += __shfl_xor_sync(0xffffffffu, s0.y, off);
-        s1.x += __shfl_xor_sync(0xffffffffu, s1.x, off);
-        s1.y += __shfl_xor_sync(0xffffffffu, s1.y, off);
-      }
-      if (lane == 0) {
-        part_s[wid][0] = s0;
-        part_s[wid][1] = s1;
-      }
+    for (int off = 16; off; off >>= 1) {
+      s0.x += __shfl_xor_sync(0xffffffffu, s0.x, off);
+      s0.y += __shfl_xor_sync(0xffffffffu, s0.y, off);
+      s1.x += __shfl_xor_sync(0xffffffffu, s1.x, off);
+      s1.y += __shfl_xor_sync(0xffffffffu, s1.y, off);
     }
-    __syncthreads();
-    if (threadIdx.x < 4) {
-      // fixed-order combination of the four quarters
-      const int sd = threadIdx.x >> 1, which = threadIdx.x & 1;
-      double2 t = part_s[4 * sd][which];
-      t = cadd(t, part_s[4 * sd + 1][which]);
-      t = cadd(t, part_s[4 * sd + 2][which]);
-      t = cadd(t, part_s[4 * sd + 3][which]);
-      S[sd][which] = t;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int i0 = 2 * p, i1 = 2 * p + 1;
-      for (int side = 0; side < 2; ++side) {
-        const bool ok = side == 0 ? okA : okB;
-        if (!ok) continue;
-        const int k = side == 0 ? kA : kB;
-        // column of k is c (side 0) or cb (side 1); partner sum from the other column
-        const double2 Zk = S[side][0];
-        const double2 Zp = cconj(S[side ^ (cb != c ? 1 : 0)][1]);
-        double2 Ya = make_double2(0.5 * (Zk.x + Zp.x), 0.5 * (Zk.y + Zp.y));
-        double2 Yb = make_double2(0.5 * (Zk.y - Zp.y), -0.5 * (Zk.x - Zp.x));
-        if (k == L) { Ya.y = 0.0; Yb.y = 0.0; }
-        double& rp = side == 0 ? rpA : rpB;
-        const double ir = side == 0 ? irA : irB;
-        const double r0 = rp, r1 = r0 * ir;
-        const double cC = r0 * (R.ac[i0] * Ya.x + R.bc[i0] * Ya.y) + r1 * (R.ac[i1] * Yb.x + R.bc[i1] * Yb.y);
-        const double cS = r0 * (R.as[i0] * Ya.x + R.bs[i0] * Ya.y) + r1 * (R.as[i1] * Yb.x + R.bs[i1] * Yb.y);
-        if (side == 0) { accA += cC; accAS += cS; } else { accB += cC; accBS += cS; }
-        rp = r1 * ir;
-      }
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    double* part = a.part + (long long)ul * a.part_stride;
-    for (int side = 0; side < 2; ++side) {
-      const bool ok = side == 0 ? okA : okB;
-      if (!ok) continue;
-      const int k = side == 0 ? kA : kB;
-      double v = side == 0 ? accA : accB;
-      if (a.cs_tab) {
-        const double2 th = __ldg(a.cs_tab + (k - 1));
-        v = v * th.x + (side == 0 ? accAS : accBS) * th.y;
-      }
-      part[k - 1] = v;
+    if (lane == 0) {
+      part_s[wid][p][0] = s0;
+      part_s[wid][p][1] = s1;
     }
   }
+  __syncthreads();
+  const int side = threadIdx.x;
+  if (side >= 2) return;
+  const bool ok = side == 0 ? okA : okB;
+  if (!ok) return;
+  const int k = side == 0 ? kA : kB;
+  const double ir = a.Ld / (double)k;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int p = a.M - 1; p >= 0; --p) {
+    // fixed-order combination of the four quarters; Z[k] from this side's
+    // column, conj Z[2L-k] from the partner column
+    const int sk = side, sp = side ^ (cb != c ? 1 : 0);
+    double2 Zk = part_s[4 * sk][p][0], Zp = part_s[4 * sp][p][1];
+#pragma unroll
+    for (int w = 1; w < 4; ++w) {
+      Zk = cadd(Zk, part_s[4 * sk + w][p][0]);
+      Zp = cadd(Zp, part_s[4 * sp + w][p][1]);
+    }
+    Zp = cconj(Zp);
+    double2 Ya = make_double2(Zk.x + Zp.x, Zk.y + Zp.y);
+    double2 Yb = make_double2(Zk.y - Zp.y, Zp.x - Zk.x);
+    if (k == L) { Ya.y = 0.0; Yb.y = 0.0; }
+    const int i0 = 2 * p, i1 = 2 * p + 1;
+    const double ac0 = R.ac[i0], bc0 = R.bc[i0], ac1 = R.ac[i1], bc1 = R.bc[i1];
+    const double t0x = fma(ac0, Ya.x, bc0 * Ya.y), t0y = fma(ac0, Ya.y, -bc0 * Ya.x);
+    const double t1x = fma(ac1, Yb.x, bc1 * Yb.y), t1y = fma(ac1, Yb.y, -bc1 * Yb.x);
+    const double w2 = ir * ir;
+    acc.x = fma(acc.x, w2, fma(ir, t1x, t0x));
+    acc.y = fma(acc.y, w2, fma(ir, t1y, t0y));
+  }
+  double post = 1.0;
+  if (R.pr) post = ipow_f((double)k / a.Ld, R.pr);
+  if (R.post_e && R.pe) post *= ipow_f(R.post_e[k - 1], R.pe);
+  const double r0 = 0.5 * post * sqrt(ir);
+  double v = acc.x * r0;
+  if (a.cs_tab) {
+    const double2 th = __ldg(a.cs_tab + (k - 1));
+    v = v * th.x + (acc.y * r0) * th.y;
+  }
+  a.part[(long long)ul * a.part_stride + (k - 1)] = v;
 }
 
 // ------------------------------------------------- pass 2, paired-lane form
@@ -655,6 +669,9 @@ static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
 }
 
 cudaError_t launch_far_colgen(const FarArgs& a, int logN1, int n_units, cudaStream_t st) {
+  note_launch(), colgen_prep_kernel<<<dim3((a.L1 + 255) / 256, n_units), 256, 0, st>>>(a);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
   const int gx = a.L2 / 2 + 1;
   switch (logN1) {
     case 1: return p2_d<2, 2>(a, gx, n_units, st);

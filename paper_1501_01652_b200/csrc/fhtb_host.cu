@@ -374,6 +374,10 @@ int fhtb_set_option(const char* key, int64_t value) {
     g_far_prune = (int)value;
     return FHTB_OK;
   }
+  if (!std::strcmp(key, "chirp_variant")) {
+    g_chirp_variant = (int)value;
+    return FHTB_OK;
+  }
   if (!std::strcmp(key, "far_variant")) {
     g_far_variant = (int)value;
     return FHTB_OK;
@@ -687,7 +691,9 @@ void plan_far(const fhtb_grid* g, const std::vector<ReqDesc>& rs, FarPlan& fp) {
       for (size_t i = 0; i < all.size(); ++i)
         if (keys[i] == key) fp.units.push_back(all[i]);
       const long long n = (long long)fp.units.size() - start;
-      const size_t ub = (key / 64 == 1) ? 0 : unit_bytes_q(g, g->logQ);
+      // narrow-column units keep only their column table (M x L1)
+      const size_t ub = (key / 64 == 1) ? (size_t)g->M * ((size_t)1 << (key % 64)) * sizeof(double2)
+                                        : unit_bytes_q(g, g->logQ);
       const long long cu = chunk_for(ub + pb, n);
       for (long long u0 = 0; u0 < n; u0 += cu) {
         fp.chunks.push_back(make_int2((int)(start + u0), (int)(start + std::min(n, u0 + cu))));
