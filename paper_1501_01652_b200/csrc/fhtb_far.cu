@@ -26,6 +26,9 @@
 //              the fused DCT/DST separation and the row epilogue.
 //   reduce:  F[vec][j] += sum of the unit partials of that vector, in unit
 //            order (deterministic).
+#include <cuda.h>
+#include <cstring>
+
 #include "fhtb_core.cuh"
 #include "fhtb_launch.h"
 
@@ -69,13 +72,18 @@ __device__ __forceinline__ void unit_cols(const FarArgs& a, const ReqDesc& R, co
 }
 
 // ------------------------------------------------------------------ pass 1
-template <int N2, int E, int W, int MINB>
+// TMA: the twiddled outputs of the CTA's W columns are staged in shared
+// memory as rows [k2][w] (reusing the FFT buffer) and written to G by 2D
+// tensor stores (boxes of 2W doubles x BR rows), so the strided W*16-byte row
+// segments do not go through the LSU path one warp instruction at a time.
+template <int N2, int E, int W, int MINB, bool TMA>
 __global__ void __launch_bounds__(W * (N2 / E), MINB)
-far_pass1_kernel(FarArgs a) {
+far_pass1_kernel(FarArgs a, const __grid_constant__ CUtensorMap gmap) {
   constexpr int T = N2 / E;
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
   constexpr int NP = N2 + PAD;
-  extern __shared__ double2 sm2[];
+  constexpr int BR = N2 < 256 ? N2 : 256;           // tensor-store box rows
+  extern __shared__ __align__(128) double2 sm2[];
   const int tid = threadIdx.x, w = tid % W, tt = tid / W;
   const int L1 = a.L1;
   const long long n1 = (long long)blockIdx.x * W + w;
@@ -115,15 +123,39 @@ far_pass1_kernel(FarArgs a) {
     const double ims = vs * iws;
     const double2 extra = make_double2(vs, ims);
     vs = ims * iws;
+    if (TMA && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     __syncthreads();
     block_fft<N2, E, 1, true>(z, sm, tt, tw, extra);
-    double2* G = a.G + ((long long)(ul * a.M + p) * N2) * L1;
+    if (TMA) {
+      __syncthreads();
 #pragma unroll
-    for (int s = 0; s < E; ++s) {
-      const int k2 = fft_out_index<N2, E>(tt, s);
-      G[(long long)k2 * L1 + n1] = cmul(z[s], qt[s * NTH]);
+      for (int s = 0; s < E; ++s) {
+        const int k2 = fft_out_index<N2, E>(tt, s);
+        sm2[k2 * W + w] = cmul(z[s], qt[s * NTH]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        const int row0 = (ul * a.M + p) * a.L2;
+        const int c0 = 2 * (int)(blockIdx.x * W);
+#pragma unroll
+        for (int r = 0; r < N2; r += BR) {
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(sm2 + r * W);
+          asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+                       :: "l"(&gmap), "r"(sa), "r"(c0), "r"(row0 + r) : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    } else {
+      double2* G = a.G + ((long long)(ul * a.M + p) * N2) * L1;
+#pragma unroll
+      for (int s = 0; s < E; ++s) {
+        const int k2 = fft_out_index<N2, E>(tt, s);
+        G[(long long)k2 * L1 + n1] = cmul(z[s], qt[s * NTH]);
+      }
     }
   }
+  if (TMA && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Pass 1, one CTA per (column group, unit, pair p): no per-element state is
@@ -620,15 +652,50 @@ __global__ void far_reduce_kernel(FarArgs a, int n_units) {
 // profiles/round1_far_variants.md).
 int g_far_variant = 20;
 
+// 2D tensor map over G viewed as rows of 2*L1 doubles (one row per (unit,
+// pair, k2)); cuTensorMapEncodeTiled is fetched through the runtime so the
+// library does not link libcuda directly.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+static bool g_tmap(CUtensorMap* m, const FarArgs& a, int n_units, int W, int BR) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || ((unsigned long long)a.G & 127)) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)2 * a.L1, (cuuint64_t)n_units * a.M * a.L2};
+  const cuuint64_t strides[1] = {(cuuint64_t)a.L1 * 16};
+  const cuuint32_t box[2] = {(cuuint32_t)(2 * W), (cuuint32_t)BR};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)a.G, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int N2, int E, int W, int MINB>
 static cudaError_t p1_t(const FarArgs& a, int n_units, cudaStream_t st) {
   constexpr int T = N2 / E;
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
-  const int smem = (W * (N2 + PAD) + W * N2) * 16;   // FFT buffers + four-step twiddles
-  auto k = far_pass1_kernel<N2, E, W, MINB>;
+  const int smem = (W * (N2 + PAD) + W * N2) * 16;   // FFT buffers (staging) + four-step twiddles
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof m);
+  const bool tma = W >= 2 && !(g_far_variant & 0x10000) && g_tmap(&m, a, n_units, W, N2 < 256 ? N2 : 256);
+  auto k = tma ? far_pass1_kernel<N2, E, W, MINB, true> : far_pass1_kernel<N2, E, W, MINB, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  note_launch(), k<<<dim3(a.L1 / W, n_units), W * T, smem, st>>>(a);
+  note_launch(), k<<<dim3(a.L1 / W, n_units), W * T, smem, st>>>(a, m);
   return cudaGetLastError();
 }
 
