@@ -121,6 +121,15 @@ size_t fhtb_apply_workspace(const fhtb_grid* g, int32_t n_req, int32_t n_vec, in
 int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C,
                int64_t ldc, int32_t n_vec, double* F, int64_t ldf, int32_t flags, void* ws,
                size_t ws_bytes, void* stream);
+/* One shard of fhtb_apply for splitting a single application over several
+ * devices: shard s of n computes the asymptotic term pairs
+ * [M s/n, M (s+1)/n) of every far-field unit and the near-field tiles
+ * t = s (mod n); the n partial results sum (e.g. ncclAllReduce) to the
+ * fhtb_apply result up to rounding.  F is accumulated into as fhtb_apply;
+ * same workspace size.  fhtb_apply == fhtb_apply_part(..., 0, 1, ...). */
+int fhtb_apply_part(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C,
+                    int64_t ldc, int32_t n_vec, double* F, int64_t ldf, int32_t flags, int32_t shard,
+                    int32_t n_shards, void* ws, size_t ws_bytes, void* stream);
 
 /* Direct sums with rank-1 arguments z = row_val[k] * col_val[n] over a full
  * n_rows x n_cols rectangle: fourier_bessel.py:148-172 (low columns),

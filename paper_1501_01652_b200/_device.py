@@ -5,6 +5,7 @@ host arrays; every numerical operation on N-length data runs in
 libfhtb200.so.
 """
 
+import contextlib
 import threading
 
 import numpy as np
@@ -14,6 +15,29 @@ from . import _lib
 
 _ws_lock = threading.Lock()
 _ws = {}
+_tls = threading.local()
+
+
+def shard():
+    """(index, count) of the work split active in this thread (default (0, 1))."""
+    return getattr(_tls, "shard", (0, 1))
+
+
+@contextlib.contextmanager
+def sharding(index, count):
+    """Within the block, every engine application computes only shard
+    `index` of `count` (fhtb_apply_part: term pairs and near-field tiles),
+    and direct (non-engine) sums run on shard 0 only; the `count` partial
+    results sum to the full transform (dist.distributed_transform)."""
+    index, count = int(index), int(count)
+    if count < 1 or not 0 <= index < count:
+        raise ValueError("bad shard index/count")
+    prev = shard()
+    _tls.shard = (index, count)
+    try:
+        yield
+    finally:
+        _tls.shard = prev
 
 
 def device():

@@ -61,6 +61,8 @@ EXPORTS = {
     "fhtb_apply_workspace": (ctypes.c_size_t, [vp, i32, i32, i32]),
     "fhtb_apply": (i32, [vp, ctypes.POINTER(Request), i32, vp, i64, i32, vp, i64, i32, vp,
                          ctypes.c_size_t, vp]),
+    "fhtb_apply_part": (i32, [vp, ctypes.POINTER(Request), i32, vp, i64, i32, vp, i64, i32, i32, i32, vp,
+                              ctypes.c_size_t, vp]),
     "fhtb_direct_workspace": (ctypes.c_size_t, [ctypes.POINTER(DirectDesc), i32, i32]),
     "fhtb_direct_apply": (i32, [ctypes.POINTER(DirectDesc), ctypes.POINTER(Request), i32, vp,
                                 i64, i32, vp, i64, i32, vp, ctypes.c_size_t, vp]),

@@ -89,7 +89,15 @@ chirp_pass1_kernel(FarArgs a) {
   double2* sm = sm2 + w * NP;
   const double2* tw = a.tw + (N2 - 2);
   const int nterm = 2 * a.M;
-  for (int i = 0; i < nterm; ++i) {
+  const int t0 = 2 * a.p0, t1 = 2 * a.p1;     // this shard's terms
+  for (int i = 0; i < t0; ++i) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      br[e] *= iw[e];
+      bi[e] *= iw[e];
+    }
+  }
+  for (int i = t0; i < t1; ++i) {
     double2 z[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -135,15 +143,16 @@ chirp_pass2_kernel(FarArgs a) {
   }
   const double2* tw = a.tw + (N1 - 2);
   const int nterm = 2 * a.M;
-  double2* row = a.G + (long long)(ul * nterm) * Q + (long long)k2 * N1;
+  const int t0 = 2 * a.p0, t1 = 2 * a.p1;     // this shard's terms
+  double2* row = a.G + (long long)(ul * nterm + t0) * Q + (long long)k2 * N1;
   double2 zn[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) zn[e] = row[tt + T * e];
-  for (int i = 0; i < nterm; ++i, row += Q) {
+  for (int i = t0; i < t1; ++i, row += Q) {
     double2 z[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) z[e] = zn[e];
-    if (i + 1 < nterm) {
+    if (i + 1 < t1) {
 #pragma unroll
       for (int e = 0; e < E; ++e) zn[e] = row[Q + tt + T * e];
     }
@@ -203,15 +212,16 @@ chirp_pass3_kernel(FarArgs a) {
   double2* sm = sm2 + w * NP;
   const double2* tw = a.tw + (N2 - 2);
   const int nterm = 2 * a.M;
-  const double2* G = a.G + (long long)(ul * nterm + nterm - 1) * Q + n1;
+  const int t0 = 2 * a.p0, t1 = 2 * a.p1;     // this shard's terms
+  const double2* G = a.G + (long long)(ul * nterm + t1 - 1) * Q + n1;
   double2 zn[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) zn[e] = G[(long long)(tt + T * e) * Q1];
-  for (int i = nterm - 1; i >= 0; --i, G -= Q) {
+  for (int i = t1 - 1; i >= t0; --i, G -= Q) {
     double2 z[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) z[e] = zn[e];
-    if (i > 0) {
+    if (i > t0) {
 #pragma unroll
       for (int e = 0; e < E; ++e) zn[e] = G[(long long)(tt + T * e) * Q1 - Q];
     }
@@ -236,7 +246,8 @@ chirp_pass3_kernel(FarArgs a) {
       double post = 1.0;
       if (R.pr) post = ipow_c((double)k / a.Ld, R.pr);
       if (R.post_e && R.pe) post *= ipow_c(R.post_e[j], R.pe);
-      const double rp0 = post * sqrt(ir[q]) * invQ;
+      double rp0 = post * sqrt(ir[q]) * invQ;
+      for (int i = 0; i < t0; ++i) rp0 *= ir[q];                  // (L/k)^{t0}
       const long long P = 2 * k0 * n0 + 2 * s * j * n0 + s * ((j * j) % (4 * L));
       const double2 oc = chirpE(P, L);
       const double2 wv = cmul(oc, SC[q]);

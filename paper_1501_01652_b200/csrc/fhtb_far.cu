@@ -111,7 +111,12 @@ far_pass1_kernel(FarArgs a, const __grid_constant__ CUtensorMap gmap) {
   constexpr int NTH = W * T;
 #pragma unroll
   for (int s = 0; s < E; ++s) qt[s * NTH] = qtw(a, n1 * fft_out_index<N2, E>(tt, s));
-  for (int p = 0; p < a.M; ++p) {
+  for (int p = 0; p < a.p0; ++p) {          // advance to the shard's first pair
+#pragma unroll
+    for (int e = 0; e < EH; ++e) v[e] = (v[e] * iw[e]) * iw[e];
+    vs = (vs * iws) * iws;
+  }
+  for (int p = a.p0; p < a.p1; ++p) {
     double2 z[E];
 #pragma unroll
     for (int e = 0; e < EH; ++e) {
@@ -173,6 +178,7 @@ far_pass1p_kernel(FarArgs a) {
   const int L1 = a.L1;
   const long long n1 = (long long)blockIdx.x * W + w;
   const int ul = blockIdx.y / a.M, p = blockIdx.y % a.M;
+  if (p < a.p0 || p >= a.p1) return;
   const UnitDesc U = a.units[a.u0 + ul];
   const ReqDesc& R = a.reqs[U.req];
   const BlockDesc& B = a.blocks[U.block];
@@ -291,8 +297,16 @@ far_pass2_kernel(FarArgs a) {
     for (int e = 0; e < E; ++e)
       tq[MODE == 2 ? e : 0] = myk2 ? qtw(a, (long long)(tt + T * e) * myk2) : make_double2(1.0, 0.0);
   }
-  for (int pi = 0; pi < a.M; ++pi) {
-    const int p = HOR ? a.M - 1 - pi : pi;
+  if (!HOR) {
+    for (int p = 0; p < a.p0; ++p) {        // advance to the shard's first pair
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[ONEPASS ? e : 0] = (v[ONEPASS ? e : 0] * iw[ONEPASS ? e : 0]) * iw[ONEPASS ? e : 0];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) rp[HOR ? 0 : q] = (rp[HOR ? 0 : q] * ir[q]) * ir[q];
+    }
+  }
+  for (int pi = 0; pi < a.p1 - a.p0; ++pi) {
+    const int p = HOR ? a.p1 - 1 - pi : a.p0 + pi;
     double2 z[E];
     if (ONEPASS) {
 #pragma unroll
@@ -362,7 +376,8 @@ far_pass2_kernel(FarArgs a) {
       double post = 1.0;
       if (R.pr) post = ipow_f((double)k / a.Ld, R.pr);
       if (R.post_e && R.pe) post *= ipow_f(R.post_e[k - 1], R.pe);
-      const double r0 = 0.5 * post * sqrt(ir[q]);
+      double r0 = 0.5 * post * sqrt(ir[q]);
+      for (int p = 0; p < a.p0; ++p) r0 = (r0 * ir[q]) * ir[q];    // (L/k)^{2 p0}
       u = make_double2(u.x * r0, u.y * r0);
     }
     if (MODE == 2 && sh) {
@@ -436,7 +451,7 @@ far_rowdot_kernel(FarArgs a, int c_lo) {
   const double2* rot = a.tw + (L1 - 2);   // e^{+2 pi i n1 / L1}
   const int qlen = (L1 + 3) / 4;
   const int lo = quarter * qlen, hi = min(L1, lo + qlen);
-  for (int p = 0; p < a.M; ++p) {
+  for (int p = a.p0; p < a.p1; ++p) {
     const double2* g = a.G + ((long long)(ul * a.M + p) * L2 + col) * L1;
     double2 s0 = make_double2(0, 0), s1 = make_double2(0, 0);
 #pragma unroll 4
@@ -465,7 +480,7 @@ far_rowdot_kernel(FarArgs a, int c_lo) {
   const int k = side == 0 ? kA : kB;
   const double ir = a.Ld / (double)k;
   double2 acc = make_double2(0.0, 0.0);
-  for (int p = a.M - 1; p >= 0; --p) {
+  for (int p = a.p1 - 1; p >= a.p0; --p) {
     // fixed-order combination of the four quarters; Z[k] from this side's
     // column, conj Z[2L-k] from the partner column
     const int sk = side, sp = side ^ (cb != c ? 1 : 0);
@@ -490,7 +505,8 @@ far_rowdot_kernel(FarArgs a, int c_lo) {
   double post = 1.0;
   if (R.pr) post = ipow_f((double)k / a.Ld, R.pr);
   if (R.post_e && R.pe) post *= ipow_f(R.post_e[k - 1], R.pe);
-  const double r0 = 0.5 * post * sqrt(ir);
+  double r0 = 0.5 * post * sqrt(ir);
+  for (int p = 0; p < a.p0; ++p) r0 = (r0 * ir) * ir;           // (L/k)^{2 p0}
   double v = acc.x * r0;
   if (a.cs_tab) {
     const double2 th = __ldg(a.cs_tab + (k - 1));
@@ -560,7 +576,10 @@ far_pass2x_kernel(FarArgs a) {
     }
   }
   const int mycol = h ? k2b : c;
-  for (int p = 0; p < a.M; ++p) {
+  for (int p = 0; p < a.p0; ++p)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) rp[q] = (rp[q] * ir[q]) * ir[q];
+  for (int p = a.p0; p < a.p1; ++p) {
     const double2* G = a.G + ((long long)(ul * a.M + p) * L2 + mycol) * N1;
     double2 z[E];
 #pragma unroll
@@ -724,6 +743,7 @@ static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
     switch ((g_far_variant >> 4) & 15) {
       case 2: return p2_t<N1, 8, MODE, 1>(a, gx, gy, st);
       case 3: return p2_t<N1, 16, MODE, 1>(a, gx, gy, st);
+      case 4: return p2_t<N1, 8, MODE, 2>(a, gx, gy, st);
       default: break;
     }
   }

@@ -757,7 +757,14 @@ size_t fhtb_apply_workspace(const fhtb_grid* g, int32_t n_req, int32_t n_vec, in
 
 int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C, int64_t ldc,
                int32_t n_vec, double* F, int64_t ldf, int32_t flags, void* ws, size_t ws_bytes, void* stream) {
+  return fhtb_apply_part(g, reqs, n_req, C, ldc, n_vec, F, ldf, flags, 0, 1, ws, ws_bytes, stream);
+}
+
+int fhtb_apply_part(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C, int64_t ldc,
+                    int32_t n_vec, double* F, int64_t ldf, int32_t flags, int32_t shard, int32_t n_shards,
+                    void* ws, size_t ws_bytes, void* stream) {
   if (!g) return fail(FHTB_EINVAL, "null grid");
+  if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(FHTB_EINVAL, "bad shard index");
   if (n_req < 0 || n_vec < 0) return fail(FHTB_EINVAL, "negative counts");
   if (n_req == 0 || n_vec == 0) return FHTB_OK;
   for (int q = 0; q < n_req; ++q)
@@ -779,7 +786,9 @@ int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
   ReqDesc* d_req = cv.take<ReqDesc>(n_req);
   CU(cudaMemcpyAsync(d_req, rs.data(), n_req * sizeof(ReqDesc), cudaMemcpyHostToDevice, st));
 
-  if ((flags & FHTB_FAR) && !g->blocks.empty()) {
+  // this shard's asymptotic term pairs [p0, p1) (all units) -- SURVEY 8(e)
+  const int p0 = (int)((long long)g->M * shard / n_shards), p1 = (int)((long long)g->M * (shard + 1) / n_shards);
+  if ((flags & FHTB_FAR) && !g->blocks.empty() && p1 > p0) {
     FarPlan fp;
     plan_far(g, rs, fp);
     const long long nu = (long long)fp.units.size();
@@ -816,6 +825,8 @@ int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
       a.cs_tab = g->cs_tab;
       a.w0_tab = g->w0_tab;
       a.iw_tab = g->iw_tab;
+      a.p0 = p0;
+      a.p1 = p1;
       if (g->direct && g->logN2 == 0) {
         a.L1 = 1 << g->logN1;
         a.L2 = 1;
@@ -907,6 +918,8 @@ int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
     na.part = part;
     na.part_stride = (long long)n_vec * kNearRT;
     na.overwrite = 0;
+    na.shard = shard;
+    na.n_shards = n_shards;
     CU(launch_near(na, (int)g->tiles.size(), (int)q0.size() - 1, max_cols, st));
     CU(launch_near_reduce(g->d_rts, (int)g->rts.size(), part, F, ldf, n_vec, 0, st));
   }

@@ -39,6 +39,7 @@ struct NearArgs {
   double* part;
   long long part_stride;         // n_vec * 64 doubles per partial slot
   int overwrite;
+  int shard, n_shards;          // tiles t with t % n_shards == shard are computed
 };
 
 struct FarArgs {
@@ -69,6 +70,7 @@ struct FarArgs {
   const double2* cs_tab;        // (cos, sin)(-gamma k pi / L) for k = 1..L (null if gamma == 0)
   const double* w0_tab;         // omega_n^{-1/2}, n = 1..L (direct mode)
   const double* iw_tab;         // 1/omega_n
+  int p0, p1;                   // pair range of this shard (direct: pairs p; chirp: terms 2p0 .. 2p1-1)
 };
 cudaError_t launch_col_tables(double* w0, double* iw, long long L, double gamma, cudaStream_t st);
 

@@ -63,6 +63,15 @@ near_kernel(NearArgs a) {
   const int nq = q1 - q0;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
+  if (a.n_shards > 1 && (int)(blockIdx.x % a.n_shards) != a.shard) {
+    // another shard's tile: contribute zeros to the partial slot (if any)
+    if (tile.part >= 0) {
+      const int v0 = a.grp_v0[g], nv = a.grp_v0[g + 1] - v0;
+      for (int e = tid; e < kRT * nv; e += kNearThreads)
+        a.part[tile.part * a.part_stride + (long long)(v0 + e / kRT) * kRT + e % kRT] = 0.0;
+    }
+    return;
+  }
 
   wmma::fragment<wmma::accumulator, 8, 8, 4, double> acc[JT / 8];
 #pragma unroll

@@ -1,13 +1,24 @@
-"""Multi-GPU batch sharding (one process per GPU, torch.distributed).
+"""Multi-GPU execution (one process per GPU, torch.distributed).
 
-The transforms of different coefficient vectors are independent
+Batches: the transforms of different coefficient vectors are independent
 (SURVEY.md 8(e)), so a batch is split into contiguous per-rank shards with
 no data-path collective; the only communication is the optional gather of
 the results (NCCL all_gather over NVLink on GPUs, gloo in the CPU tests).
+
+One transform over several GPUs: the T = 2M(2P+1) asymptotic DCT/DST pairs
+and the near-field tiles of an application are independent, so every rank
+runs the whole call with the work split of _device.sharding (rank r of W
+computes term pairs [M r/W, M (r+1)/W) of every block and near-field tiles
+t = r mod W; direct sums on rank 0) and the partial outputs are summed by
+one all-reduce (NCCL over NVLink/NVSwitch) -- the "shard the pairs, then
+reduce" form of SURVEY.md 8(e).
 """
 
+import numpy as np
 import torch
 import torch.distributed as dist
+
+from . import _device
 
 
 def shard_range(n_items, rank, world):
@@ -41,3 +52,30 @@ def sharded_transform(fn, C, group=None, gather=True):
     lo, hi = shard_range(C.shape[0], rank, world)
     out = fn(C[lo:hi])
     return gather_rows(out, C.shape[0], group) if gather else out
+
+
+def distributed_transform(fn, *args, group=None, **kwargs):
+    """Evaluate ONE transform call fn(*args, **kwargs) (e.g.
+    schlomilch_fast(params, c)) split across the ranks of `group`; every rank
+    passes the same arguments and receives the full result (sum of the rank
+    partials).  Pass CUDA tensors to keep the result on the device; a numpy
+    result is reduced through a tensor on the backend's device."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return fn(*args, **kwargs)
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    with _device.sharding(rank, world):
+        out = fn(*args, **kwargs)
+    if isinstance(out, torch.Tensor):
+        dist.all_reduce(out, group=group)
+        return out
+    arr = np.asarray(out)
+    on_gpu = dist.get_backend(group) == "nccl"
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    if on_gpu:
+        t = t.to(_device.device())
+    if t.is_complex():
+        t = torch.view_as_real(t)
+        dist.all_reduce(t, group=group)
+        return torch.view_as_complex(t).cpu().numpy()
+    dist.all_reduce(t, group=group)
+    return t.cpu().numpy()

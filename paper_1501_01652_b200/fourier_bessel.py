@@ -110,8 +110,15 @@ def _bump(stats, key, amount=1):
 
 
 def _direct_apply(row_val, col_val, n_cols, orders, requests, C, F, overwrite=False, r_scale=1.0):
-    """Direct rank-1-argument sums on the device (fhtb_direct_apply)."""
+    """Direct rank-1-argument sums on the device (fhtb_direct_apply).  Under
+    a work split (_device.sharding) only shard 0 computes them; the others
+    contribute zeros (an overwrite leaves zeros)."""
     if not requests:
+        return F
+    s, _ = _device.shard()
+    if s != 0:
+        if overwrite:
+            F.zero_()
         return F
     from .schlomilch import _pack_requests
     lib = _lib.load()

@@ -176,9 +176,10 @@ class _Grid:
         arr, keep = _pack_requests(requests)
         ws_n = self._lib.fhtb_apply_workspace(self.handle, len(requests), C.shape[0], flags)
         ws = _device.workspace(ws_n)
-        _lib.check(self._lib.fhtb_apply(self.handle, arr, len(requests), _device.ptr(C), C.stride(0),
-                                        C.shape[0], _device.ptr(F), F.stride(0), flags, _device.ptr(ws),
-                                        ws.numel(), _device.stream_ptr()))
+        s, n = _device.shard()
+        _lib.check(self._lib.fhtb_apply_part(self.handle, arr, len(requests), _device.ptr(C), C.stride(0),
+                                             C.shape[0], _device.ptr(F), F.stride(0), flags, s, n,
+                                             _device.ptr(ws), ws.numel(), _device.stream_ptr()))
         del keep
         return F
 

@@ -72,3 +72,67 @@ def test_two_rank_sharded_transform(n_items):
     res = dict(q.get(timeout=10) for _ in range(2))
     assert res == {0: True, 1: True}
     assert all(p.exitcode == 0 for p in procs)
+
+
+# ----------------------------------------------- one transform over the ranks
+def _split_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import numpy as np
+
+        from paper_1501_01652_b200 import _device
+        from paper_1501_01652_b200.dist import distributed_transform
+
+        terms = torch.arange(1, 11, dtype=torch.float64)            # 10 "pairs"
+        seen = []
+
+        def fn(scale, as_numpy=False):
+            # stand-in for an engine call: contributes the pairs of its shard
+            s, n = _device.shard()
+            seen.append((s, n))
+            lo, hi = (len(terms) * s) // n, (len(terms) * (s + 1)) // n
+            part = torch.zeros(4, dtype=torch.float64)
+            part += scale * terms[lo:hi].sum()
+            if s == 0:
+                part[0] += 100.0                                      # "direct" part on shard 0 only
+            return part.numpy() if as_numpy else part
+
+        full = torch.full((4,), 2.0 * terms.sum().item())
+        full[0] += 100.0
+        out_t = distributed_transform(fn, 2.0)
+        out_n = distributed_transform(fn, 2.0, as_numpy=True)
+        ok = torch.equal(out_t, full) and np.array_equal(out_n, full.numpy())
+        ok = ok and seen == [(rank, world), (rank, world)] and _device.shard() == (0, 1)
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_split_single_transform():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    res = dict(q.get(timeout=10) for _ in range(2))
+    assert res == {0: True, 1: True}
+    assert all(p.exitcode == 0 for p in procs)
+
+
+def test_sharding_context_validation():
+    from paper_1501_01652_b200 import _device
+
+    with pytest.raises(ValueError):
+        with _device.sharding(2, 2):
+            pass
+    with _device.sharding(1, 3):
+        assert _device.shard() == (1, 3)
+        with _device.sharding(0, 2):
+            assert _device.shard() == (0, 2)
+        assert _device.shard() == (1, 3)
+    assert _device.shard() == (0, 1)

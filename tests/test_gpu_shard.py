@@ -1,0 +1,82 @@
+"""One transform split over W workers (dist.distributed_transform).
+
+On the single GPU of the test box the W shards run one after the other in
+this process (_device.sharding); their sum must equal the unsplit transform
+to rounding, for every far-field form (one-pass, pruned two-pass, chirp-z)
+and for the nested Fourier-Bessel / DHT drivers (direct parts on shard 0,
+the DHT's overwritten rows zero elsewhere).  W = 1 is the plain call,
+bitwise.  The NCCL all-reduce itself is covered by the gloo test in
+test_dist.py.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1501_01652_b200 as fh
+from paper_1501_01652_b200 import _device
+
+pytestmark = pytest.mark.gpu
+
+
+def _split_sum(fn, world):
+    parts = []
+    for s in range(world):
+        with _device.sharding(s, world):
+            parts.append(fn().clone())
+    return torch.stack(parts).sum(0)
+
+
+def _close(a, b, c, eps=1e-15):
+    tol = 2 * eps * float(np.abs(np.asarray(c)).sum()) + 1e-300
+    return float((a - b).abs().max()) <= tol
+
+
+@pytest.mark.parametrize("n", [1024, 8192, 3000])          # one-pass, two-pass (pruned), chirp-z
+@pytest.mark.parametrize("world", [2, 3, 7])
+def test_schlomilch_split_sums_to_full(cuda_dev, n, world):
+    rng = np.random.default_rng([5, n])
+    c = torch.from_numpy(rng.standard_normal((2, n)) / np.arange(1, n + 1)).to(cuda_dev)
+    params = fh.select_params(4, n, 1e-15, gamma=4.0)
+    fn = lambda: fh.schlomilch_fast(params, c)
+    full = fn()
+    assert _close(_split_sum(fn, world), full, c[0].cpu().numpy() + c[1].cpu().numpy())
+
+
+def test_single_shard_is_plain_call(cuda_dev):
+    c = torch.from_numpy(np.random.default_rng(2).standard_normal(8192)).to(cuda_dev)
+    params = fh.select_params(0, 8192, 1e-15)
+    plain = fh.schlomilch_fast(params, c)
+    with _device.sharding(0, 1):
+        one = fh.schlomilch_fast(params, c)
+    assert torch.equal(plain, one)
+
+
+def test_fourier_bessel_split(cuda_dev):
+    n = 3000
+    roots = fh.bessel_roots_j0(n)
+    c = torch.from_numpy(np.random.default_rng(9).uniform(-1, 1, n)).to(cuda_dev)
+    fn = lambda: fh.fourier_bessel_eval(0, c, 1e-12, roots=roots)
+    full = fn()
+    assert _close(_split_sum(fn, 3), full, c.cpu().numpy(), eps=1e-12)
+
+
+def test_dht_split(cuda_dev):
+    n = 600
+    plan = fh.dht_plan(n, 1e-15)
+    c = torch.from_numpy(np.random.default_rng(4).standard_normal(n)).to(cuda_dev)
+    fn = lambda: fh.dht(plan, c)
+    full = fn()
+    assert _close(_split_sum(fn, 2), full, c.cpu().numpy())
+    # rows <= row_split come from the direct sums of shard 0 only
+    with _device.sharding(1, 2):
+        other = fn()
+    assert float(other[: plan.row_split].abs().max()) == 0.0
+
+
+def test_distributed_transform_single_process(cuda_dev):
+    from paper_1501_01652_b200.dist import distributed_transform
+
+    c = torch.from_numpy(np.random.default_rng(1).standard_normal(4096)).to(cuda_dev)
+    params = fh.select_params(0, 4096, 1e-8)
+    assert torch.equal(distributed_transform(fh.schlomilch_fast, params, c), fh.schlomilch_fast(params, c))

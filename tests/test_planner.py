@@ -176,7 +176,7 @@ def test_public_surface_matches_reference():
                 "schlomilch_single_partition", "schlomilch_fast", "NeumannParams", "neumann_column_cutoff",
                 "taylor_column_cutoff", "select_neumann_params", "neumann_matvec", "fourier_bessel_eval",
                 "fourier_bessel_direct", "DhtPlan", "dht_plan", "dht", "dht_direct",
-                "dht_self_inverse_residual", "__version__"}
+                "dht_self_inverse_residual", "VectorFileError", "read_vector", "write_vector", "__version__"}
     assert expected <= names
     for n in expected - {"__version__"}:
         assert hasattr(fh, n)
