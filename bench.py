@@ -373,7 +373,8 @@ def traffic_from_profile():
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get("far_pass_pair_bytes_per_vector")
+            t = json.load(f)
+            return t.get("far_field_dram_bytes_per_vector", t.get("far_pass_pair_bytes_per_vector"))
     except Exception:
         return None
 
