@@ -131,6 +131,31 @@ int fhtb_apply_part(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req,
                     int64_t ldc, int32_t n_vec, double* F, int64_t ldf, int32_t flags, int32_t shard,
                     int32_t n_shards, void* ws, size_t ws_bytes, void* stream);
 
+/* Distributed four-step (exchange mode) -- SURVEY 8(e): one application
+ * split over `world` ranks where the full (unpruned) far-field blocks of a
+ * power-of-two grid run as a distributed FFT: rank r computes pass 1 for its
+ * column slab n1 in [r L1/world, (r+1) L1/world) into `send`, laid out as
+ * world equal chunks (one per destination rank: the rows k2 of the column
+ * pairs {c, L2-c} that rank owns); the library then calls
+ * exchange(user, round, bytes_per_peer), which must perform the all-to-all
+ * (recv chunk s <- chunk r of rank s's send, e.g. ncclAllToAll or
+ * dist.all_to_all_single) ordered on `stream`; pass 2 of rank r's column pairs
+ * reads `recv`.  Pruned side blocks and near-field tiles are split as in
+ * fhtb_apply_part; the world partial F sum to the fhtb_apply result up to
+ * rounding.  xbytes = size of send (== size of recv), a multiple of
+ * fhtb_apply_x_unit_bytes (units per exchange round); workspace from
+ * fhtb_apply_x_workspace.  Grids without full two-pass blocks (one-pass,
+ * chirp) or with L1 not divisible into 16-column slabs never call
+ * exchange (plain fhtb_apply_part split); unit_bytes is then 0. */
+typedef int (*fhtb_exchange_fn)(void* user, int32_t round, size_t bytes_per_peer);
+size_t fhtb_apply_x_unit_bytes(const fhtb_grid* g, int32_t world);
+size_t fhtb_apply_x_workspace(const fhtb_grid* g, int32_t n_req, int32_t n_vec, int32_t flags, int32_t world,
+                              size_t xbytes);
+int fhtb_apply_x(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C, int64_t ldc,
+                 int32_t n_vec, double* F, int64_t ldf, int32_t flags, int32_t rank, int32_t world, void* send,
+                 void* recv, size_t xbytes, fhtb_exchange_fn exchange, void* user, void* ws, size_t ws_bytes,
+                 void* stream);
+
 /* Direct sums with rank-1 arguments z = row_val[k] * col_val[n] over a full
  * n_rows x n_cols rectangle: fourier_bessel.py:148-172 (low columns),
  * dht.py:82-94 (direct rows), and the O(N^2) oracles schlomilch.py:223-229,

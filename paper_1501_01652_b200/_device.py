@@ -23,21 +23,35 @@ def shard():
     return getattr(_tls, "shard", (0, 1))
 
 
+def shard_exchange():
+    """The all-to-all callable of the active split, or None (pair split)."""
+    return getattr(_tls, "exchange", None)
+
+
 @contextlib.contextmanager
-def sharding(index, count):
+def sharding(index, count, exchange=None):
     """Within the block, every engine application computes only shard
-    `index` of `count` (fhtb_apply_part: term pairs and near-field tiles),
-    and direct (non-engine) sums run on shard 0 only; the `count` partial
-    results sum to the full transform (dist.distributed_transform)."""
+    `index` of `count`, and direct (non-engine) sums run on shard 0 only; the
+    `count` partial results sum to the full transform
+    (dist.distributed_transform).
+
+    exchange=None: fhtb_apply_part (term pairs and near-field tiles).
+    exchange=fn:   fhtb_apply_x -- full far-field blocks of power-of-two grids
+                   as a distributed four-step FFT; fn(send, recv, bytes_per_peer)
+                   must perform the all-to-all of the uint8 CUDA buffers
+                   (count equal chunks of bytes_per_peer each) in stream order.
+    """
     index, count = int(index), int(count)
     if count < 1 or not 0 <= index < count:
         raise ValueError("bad shard index/count")
-    prev = shard()
+    prev, prev_x = shard(), shard_exchange()
     _tls.shard = (index, count)
+    _tls.exchange = exchange
     try:
         yield
     finally:
         _tls.shard = prev
+        _tls.exchange = prev_x
 
 
 def device():

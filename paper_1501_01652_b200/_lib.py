@@ -41,6 +41,9 @@ class DirectDesc(ctypes.Structure):
                 ("n_data_cols", i64), ("r_scale", f64), ("n_orders", i32), ("orders", P_i32)]
 
 
+# int exchange(void* user, int32 round, size_t bytes_per_peer)  (fhtb_exchange_fn)
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t)
+
 EXPORTS = {
     "fhtb_abi_version": (i32, []),
     "fhtb_last_error": (ctypes.c_char_p, []),
@@ -63,6 +66,10 @@ EXPORTS = {
                          ctypes.c_size_t, vp]),
     "fhtb_apply_part": (i32, [vp, ctypes.POINTER(Request), i32, vp, i64, i32, vp, i64, i32, i32, i32, vp,
                               ctypes.c_size_t, vp]),
+    "fhtb_apply_x_unit_bytes": (ctypes.c_size_t, [vp, i32]),
+    "fhtb_apply_x_workspace": (ctypes.c_size_t, [vp, i32, i32, i32, i32, ctypes.c_size_t]),
+    "fhtb_apply_x": (i32, [vp, ctypes.POINTER(Request), i32, vp, i64, i32, vp, i64, i32, i32, i32, vp, vp,
+                           ctypes.c_size_t, EXCHANGE_FN, vp, vp, ctypes.c_size_t, vp]),
     "fhtb_direct_workspace": (ctypes.c_size_t, [ctypes.POINTER(DirectDesc), i32, i32]),
     "fhtb_direct_apply": (i32, [ctypes.POINTER(DirectDesc), ctypes.POINTER(Request), i32, vp,
                                 i64, i32, vp, i64, i32, vp, ctypes.c_size_t, vp]),

@@ -86,7 +86,7 @@ far_pass1_kernel(FarArgs a, const __grid_constant__ CUtensorMap gmap) {
   extern __shared__ __align__(128) double2 sm2[];
   const int tid = threadIdx.x, w = tid % W, tt = tid / W;
   const int L1 = a.L1;
-  const long long n1 = (long long)blockIdx.x * W + w;
+  const long long n1 = a.xn1 + (long long)blockIdx.x * W + w;
   const int ul = blockIdx.y;
   const UnitDesc U = a.units[a.u0 + ul];
   const ReqDesc& R = a.reqs[U.req];
@@ -150,6 +150,15 @@ far_pass1_kernel(FarArgs a, const __grid_constant__ CUtensorMap gmap) {
                        :: "l"(&gmap), "r"(sa), "r"(c0), "r"(row0 + r) : "memory");
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    } else if (a.xw) {
+      // exchange mode: row k2 goes to its owner's chunk, at the owner's row j
+      const long long nl = n1 - a.xn1;
+#pragma unroll
+      for (int s = 0; s < E; ++s) {
+        const int k2 = fft_out_index<N2, E>(tt, s);
+        const int2 oj = __ldg(a.xrow + k2);
+        a.G[oj.x * a.xchunk + (((long long)(ul * a.M + p) * a.xrows + oj.y) << a.xlog) + nl] = cmul(z[s], qt[s * NTH]);
       }
     } else {
       double2* G = a.G + ((long long)(ul * a.M + p) * N2) * L1;
@@ -231,11 +240,14 @@ far_pass1p_kernel(FarArgs a) {
 // Horner's rule over the pairs from the last one down (MODE 0 / 2; MODE 1
 // generates its columns by a forward recurrence and keeps r explicitly);
 // r_0 and the MODE-2 column-shift phase phi_k are applied once at the end.
+// MODE 3: MODE 0 in exchange mode (distributed four-step): column pairs from
+//         a.xc0, rows assembled from the received chunks of all ranks.
 template <int N1, int E, int MODE, int MINB>
 __global__ void __launch_bounds__((MODE == 1 ? 1 : 2) * (N1 / E), MINB)
 far_pass2_kernel(FarArgs a) {
   constexpr bool ONEPASS = (MODE == 1);
   constexpr bool HOR = (MODE != 1);
+  constexpr bool XCH = (MODE == 3);
   constexpr int T = N1 / E;
   constexpr int NCOL = ONEPASS ? 1 : 2;
   constexpr int NT = NCOL * T;
@@ -247,7 +259,7 @@ far_pass2_kernel(FarArgs a) {
   const int tid = threadIdx.x, h = tid / T, tt = tid % T;
   const int L = (int)a.L;
   const int L2 = a.L2;
-  const int k2a = blockIdx.x, k2b = (L2 - k2a) % L2;
+  const int k2a = XCH ? a.xc0 + (int)blockIdx.x : (int)blockIdx.x, k2b = (L2 - k2a) % L2;
   const bool selfp = (k2a == k2b);
   const int myk2 = h == 0 ? k2a : k2b;
   const int ul = blockIdx.y;
@@ -255,6 +267,7 @@ far_pass2_kernel(FarArgs a) {
   const ReqDesc& R = a.reqs[U.req];
   const BlockDesc& B = a.blocks[U.block];
   const double2* tw = a.tw + (N1 - 2);
+  const int xj = XCH ? __ldg(a.xrow + myk2).y : 0;
 
   int kq[NQ];
   double ir[NQ], rp[HOR ? 1 : NQ];
@@ -319,6 +332,15 @@ far_pass2_kernel(FarArgs a) {
       const double2* u = a.G + (long long)(ul * a.M + p) * N1;
 #pragma unroll
       for (int e = 0; e < E; ++e) z[e] = cmul(u[tt + T * e], tq[MODE == 2 ? e : 0]);
+    } else if (XCH) {
+      // row myk2 assembled from the chunks of all source ranks
+      const long long row = ((long long)(ul * a.M + p) * a.xrows + xj) << a.xlog;
+      const int msk = (1 << a.xlog) - 1;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int n1 = tt + T * e;
+        z[e] = a.xin[(n1 >> a.xlog) * a.xchunk + row + (n1 & msk)];
+      }
     } else {
       const double2* G = a.G + ((long long)(ul * a.M + p) * L2 + myk2) * N1;
 #pragma unroll
@@ -710,11 +732,13 @@ static cudaError_t p1_t(const FarArgs& a, int n_units, cudaStream_t st) {
   const int smem = (W * (N2 + PAD) + W * N2) * 16;   // FFT buffers (staging) + four-step twiddles
   CUtensorMap m;
   std::memset(&m, 0, sizeof m);
-  const bool tma = W >= 2 && !(g_far_variant & 0x10000) && g_tmap(&m, a, n_units, W, N2 < 256 ? N2 : 256);
+  const bool tma = W >= 2 && !a.xw && !(g_far_variant & 0x10000) && g_tmap(&m, a, n_units, W, N2 < 256 ? N2 : 256);
   auto k = tma ? far_pass1_kernel<N2, E, W, MINB, true> : far_pass1_kernel<N2, E, W, MINB, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  note_launch(), k<<<dim3(a.L1 / W, n_units), W * T, smem, st>>>(a, m);
+  const int cols = a.xw ? a.L1 / a.xw : a.L1;      // exchange mode: this rank's column slab
+  if (cols % W) return cudaErrorInvalidValue;
+  note_launch(), k<<<dim3(cols / W, n_units), W * T, smem, st>>>(a, m);
   return cudaGetLastError();
 }
 
@@ -750,7 +774,7 @@ static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
   // narrow-column blocks carry a complex state per element: 8 points/thread
   constexpr int E = MODE == 2 ? (N1 >= 8 ? 8 : N1) : (N1 >= 16 ? 16 : N1);
   // two columns of 2048 with E = 16: 256 threads, 2 CTAs/SM measured best
-  constexpr int MINB = (MODE == 0 && N1 == 2048) ? 2
+  constexpr int MINB = ((MODE == 0 || MODE == 3) && N1 == 2048) ? 2
                        : (MODE == 2 && N1 <= 1024) ? (N1 <= 512 ? 4 : 2) : 1;
   return p2_t<N1, E, MODE, MINB>(a, gx, gy, st);
 }
@@ -806,7 +830,7 @@ static cudaError_t p1p_d(const FarArgs& a, int n_units, cudaStream_t st) {
 }
 
 cudaError_t launch_far_pass1(const FarArgs& a, int logN2, int n_units, cudaStream_t st) {
-  if (((g_far_variant >> 12) & 15) && a.w0_tab) {
+  if (((g_far_variant >> 12) & 15) && a.w0_tab && !a.xw) {
     switch (logN2) {
       case 6: return p1p_d<64>(a, n_units, st);
       case 7: return p1p_d<128>(a, n_units, st);
@@ -860,6 +884,18 @@ static cudaError_t p2x_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
     case 4: return p2x_t<N1, 8, 2>(a, gx, gy, st);
     default: return p2x_t<N1, 16, 1>(a, gx, gy, st);
   }
+}
+
+cudaError_t launch_far_pass2x_range(const FarArgs& a, int logN1, int n_pairs, int n_units, cudaStream_t st) {
+  switch (logN1) {
+    case 7: return p2_d<128, 3>(a, n_pairs, n_units, st);
+    case 8: return p2_d<256, 3>(a, n_pairs, n_units, st);
+    case 9: return p2_d<512, 3>(a, n_pairs, n_units, st);
+    case 10: return p2_d<1024, 3>(a, n_pairs, n_units, st);
+    case 11: return p2_d<2048, 3>(a, n_pairs, n_units, st);
+    case 12: return p2_d<4096, 3>(a, n_pairs, n_units, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_far_pass2(const FarArgs& a, int logN1, int n_units, cudaStream_t st) {

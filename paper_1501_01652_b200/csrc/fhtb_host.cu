@@ -651,7 +651,9 @@ struct FarPlan {
   size_t part_bytes = 0;                       // chirp partials
 };
 
-void plan_far(const fhtb_grid* g, const std::vector<ReqDesc>& rs, FarPlan& fp) {
+// skip_full: leave out the full (dmode 0) units of a direct two-pass grid
+// (exchange mode computes them by the distributed four-step).
+void plan_far(const fhtb_grid* g, const std::vector<ReqDesc>& rs, FarPlan& fp, int skip_full = 0) {
   fp = FarPlan();
   const int nb = (int)g->blocks.size() / 4;
   const int n_req = (int)rs.size();
@@ -663,6 +665,7 @@ void plan_far(const fhtb_grid* g, const std::vector<ReqDesc>& rs, FarPlan& fp) {
       const long long c1 = std::min<long long>(g->blocks[4 * b + 3], g->n_data_cols + 1);
       if (r1 <= r0 || c1 <= c0) continue;
       if (!g->direct && g->bdesc[b].J == 0) continue;
+      if (skip_full && g->direct && g->logN2 > 0 && g->bdesc[b].dmode == 0) continue;
       all.push_back(UnitDesc{q, b, rs[q].vec, 0});
     }
   if (g->direct) {
@@ -746,6 +749,66 @@ size_t ws_need(const fhtb_grid* g, int n_req, int n_vec, int flags) {
   return s + 4096;
 }
 
+// ------------------------------------------ distributed four-step (exchange)
+struct XCtx {
+  void* send;
+  void* recv;
+  size_t bytes;
+  fhtb_exchange_fn exchange;
+  void* user;
+};
+
+// Column-pair ownership: pairs c = 0..L2/2 ({c, L2-c}) split into balanced
+// contiguous ranges; rank s's rows are k2 = c (j = c - lo) then k2 = L2 - c
+// (j = cnt + c - lo) for the c with a distinct partner.
+void x_pairs(int L2, int world, int s, int* lo, int* cnt) {
+  const int n = L2 / 2 + 1, base = n / world, extra = n % world;
+  *lo = s * base + std::min(s, extra);
+  *cnt = base + (s < extra ? 1 : 0);
+}
+
+bool x_supported(const fhtb_grid* g, int world, int* l1, int* rows) {
+  if (!g || world < 2 || !g->direct || g->logN2 == 0) return false;
+  const int L1 = 1 << g->logN1, L2 = 1 << (g->logQ - g->logN1);
+  if (L1 % world || (L1 / world) % 16 || L2 / 2 + 1 < world) return false;
+  int lo, cnt, mx = 0;
+  for (int s = 0; s < world; ++s) {
+    x_pairs(L2, world, s, &lo, &cnt);
+    mx = std::max(mx, cnt);
+  }
+  *l1 = g->logN1;
+  *rows = 2 * mx;
+  return true;
+}
+
+std::vector<UnitDesc> x_units(const fhtb_grid* g, const std::vector<ReqDesc>& rs) {
+  std::vector<UnitDesc> u;
+  const int nb = (int)g->blocks.size() / 4;
+  for (int q = 0; q < (int)rs.size(); ++q)
+    for (int b = 0; b < nb; ++b) {
+      const long long r0 = g->blocks[4 * b], r1 = g->blocks[4 * b + 1];
+      const long long c0 = std::max<long long>(g->blocks[4 * b + 2], rs[q].col_lo);
+      const long long c1 = std::min<long long>(g->blocks[4 * b + 3], g->n_data_cols + 1);
+      if (r1 <= r0 || c1 <= c0 || g->bdesc[b].dmode != 0) continue;
+      u.push_back(UnitDesc{q, b, rs[q].vec, 0});
+    }
+  return u;
+}
+
+size_t x_ws(const fhtb_grid* g, int n_req, int world, size_t xbytes) {
+  int l1, rows;
+  if (!x_supported(g, world, &l1, &rows)) return 0;
+  const size_t per = (size_t)world * g->M * rows * ((1 << l1) / world) * sizeof(double2);
+  const size_t u_round = std::max<size_t>(1, xbytes / std::max<size_t>(per, 1));
+  const size_t nu = (size_t)std::max(n_req, 1) * (g->blocks.size() / 4 + 1);
+  return align_up(sizeof(UnitDesc) * nu) + align_up(sizeof(int2) * ((size_t)1 << (g->logQ - l1))) +
+         align_up(sizeof(double) * u_round * (size_t)g->n_out) + 4096;
+}
+
+int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C, int64_t ldc,
+               int32_t n_vec, double* F, int64_t ldf, int32_t flags, int32_t shard, int32_t n_shards,
+               const XCtx* xc, void* ws, size_t ws_bytes, void* stream);
+
 }  // namespace
 
 extern "C" {
@@ -763,13 +826,136 @@ int fhtb_apply(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
 int fhtb_apply_part(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C, int64_t ldc,
                     int32_t n_vec, double* F, int64_t ldf, int32_t flags, int32_t shard, int32_t n_shards,
                     void* ws, size_t ws_bytes, void* stream) {
+  return apply_impl(g, reqs, n_req, C, ldc, n_vec, F, ldf, flags, shard, n_shards, nullptr, ws, ws_bytes, stream);
+}
+
+size_t fhtb_apply_x_workspace(const fhtb_grid* g, int32_t n_req, int32_t n_vec, int32_t flags, int32_t world,
+                              size_t xbytes) {
+  if (!g) return 0;
+  return ws_need(g, n_req, n_vec, flags) + x_ws(g, n_req, world, xbytes);
+}
+
+size_t fhtb_apply_x_unit_bytes(const fhtb_grid* g, int32_t world) {
+  int l1, rows;
+  if (!x_supported(g, world, &l1, &rows)) return 0;
+  return (size_t)world * (size_t)g->M * (size_t)rows * (size_t)((1 << l1) / world) * sizeof(double2);
+}
+
+int fhtb_apply_x(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C, int64_t ldc,
+                 int32_t n_vec, double* F, int64_t ldf, int32_t flags, int32_t rank, int32_t world, void* send,
+                 void* recv, size_t xbytes, fhtb_exchange_fn exchange, void* user, void* ws, size_t ws_bytes,
+                 void* stream) {
+  if (!exchange || !send || !recv) return fail(FHTB_EINVAL, "exchange mode needs buffers and a callback");
+  XCtx x{send, recv, xbytes, exchange, user};
+  return apply_impl(g, reqs, n_req, C, ldc, n_vec, F, ldf, flags, rank, world, &x, ws, ws_bytes, stream);
+}
+
+}  // extern "C"
+
+namespace {
+
+// Full (dmode 0) far-field units by the distributed four-step: per round of
+// units, pass 1 over this rank's column slab into the send buffer (rows
+// grouped by owning rank), the caller's exchange (all-to-all), pass 2 over
+// this rank's column pairs from the receive buffer, reduction into F.
+int run_exchange(const fhtb_grid* g, DevCtx* ctx, const std::vector<ReqDesc>& rs, const ReqDesc* d_req,
+                 const double* C, int64_t ldc, double* F, int64_t ldf, int rank, int world, int l1, int rows,
+                 const XCtx& xc, Carve& cv, cudaStream_t st) {
+  std::vector<UnitDesc> units = x_units(g, rs);
+  const int n = (int)units.size();
+  if (n == 0) return FHTB_OK;
+  const int l2 = g->logQ - l1, L1 = 1 << l1, L2 = 1 << l2, cols = L1 / world;
+  const long long per = (long long)g->M * rows * cols;                       // elements per unit per peer
+  const long long U = (long long)(xc.bytes / ((size_t)world * per * sizeof(double2)));
+  if (U < 1) return fail(FHTB_EINVAL, "exchange buffers too small for one unit");
+  std::vector<int2> xrow(L2);
+  for (int s = 0; s < world; ++s) {
+    int lo, cnt;
+    x_pairs(L2, world, s, &lo, &cnt);
+    for (int c = lo; c < lo + cnt; ++c) {
+      xrow[c] = make_int2(s, c - lo);
+      const int p = (L2 - c) % L2;
+      if (p != c) xrow[p] = make_int2(s, cnt + c - lo);
+    }
+  }
+  UnitDesc* d_units = cv.take<UnitDesc>(n);
+  int2* d_xrow = cv.take<int2>(L2);
+  double* part = cv.take<double>((size_t)std::min<long long>(U, n) * g->n_out);
+  if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small (exchange mode)");
+  CU(cudaMemcpyAsync(d_units, units.data(), n * sizeof(UnitDesc), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_xrow, xrow.data(), L2 * sizeof(int2), cudaMemcpyHostToDevice, st));
+  FarArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.L = g->L;
+  a.M = g->M;
+  a.gamma = g->gamma;
+  a.Ld = (double)g->L;
+  a.pi_over_L = M_PI / (double)g->L;
+  a.first = g->first;
+  a.stride = g->stride;
+  a.n_out = g->n_out;
+  a.n_data_cols = g->n_data_cols;
+  a.units = d_units;
+  a.reqs = d_req;
+  a.blocks = g->d_blocks;
+  a.C = C;
+  a.ldc = ldc;
+  a.F = F;
+  a.ldf = ldf;
+  a.tw = ctx->tw;
+  a.part = part;
+  a.part_stride = g->n_out;
+  a.cs_tab = g->cs_tab;
+  a.w0_tab = g->w0_tab;
+  a.iw_tab = g->iw_tab;
+  a.p0 = 0;
+  a.p1 = g->M;
+  a.L1 = L1;
+  a.L2 = L2;
+  a.logQ = g->logQ;
+  double2 *ql, *qh;
+  int qb;
+  if (int r = get_qtab(ctx, g->logQ, &ql, &qh, &qb)) return r;
+  a.qlo = ql;
+  a.qhi = qh;
+  a.qbits = qb;
+  a.xw = world;
+  a.xlog = ilog2ll(cols);
+  a.xrows = rows;
+  a.xn1 = (long long)rank * cols;
+  a.xchunk = U * per;
+  a.xrow = d_xrow;
+  int lo, cnt;
+  x_pairs(L2, world, rank, &lo, &cnt);
+  for (int r0 = 0, round = 0; r0 < n; r0 += (int)U, ++round) {
+    const int nu = (int)std::min<long long>(U, n - r0);
+    a.u0 = r0;
+    a.G = (double2*)xc.send;
+    a.xc0 = 0;
+    CU(launch_far_pass1(a, l2, nu, st));
+    if (int r = xc.exchange(xc.user, round, (size_t)a.xchunk * sizeof(double2)))
+      return fail(FHTB_ECUDA, "exchange callback failed (" + std::to_string(r) + ")");
+    a.G = nullptr;
+    a.xin = (const double2*)xc.recv;
+    a.xc0 = lo;
+    CU(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)nu * g->n_out, st));
+    if (cnt > 0) CU(launch_far_pass2x_range(a, l1, cnt, nu, st));
+    CU(launch_far_reduce(a, nu, st));
+  }
+  return FHTB_OK;
+}
+
+int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C, int64_t ldc,
+               int32_t n_vec, double* F, int64_t ldf, int32_t flags, int32_t shard, int32_t n_shards,
+               const XCtx* xc, void* ws, size_t ws_bytes, void* stream) {
   if (!g) return fail(FHTB_EINVAL, "null grid");
   if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(FHTB_EINVAL, "bad shard index");
   if (n_req < 0 || n_vec < 0) return fail(FHTB_EINVAL, "negative counts");
   if (n_req == 0 || n_vec == 0) return FHTB_OK;
   for (int q = 0; q < n_req; ++q)
     if (reqs[q].vec < 0 || reqs[q].vec >= n_vec) return fail(FHTB_EINVAL, "request vec out of range");
-  if (ws_bytes < ws_need(g, n_req, n_vec, flags)) return fail(FHTB_EINVAL, "workspace too small");
+  const size_t need = ws_need(g, n_req, n_vec, flags) + (xc ? x_ws(g, n_req, n_shards, xc->bytes) : 0);
+  if (ws_bytes < need) return fail(FHTB_EINVAL, "workspace too small");
   DevCtx* ctx;
   if (int r = get_ctx(&ctx)) return r;
   cudaStream_t st = S(stream);
@@ -788,9 +974,14 @@ int fhtb_apply_part(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req,
 
   // this shard's asymptotic term pairs [p0, p1) (all units) -- SURVEY 8(e)
   const int p0 = (int)((long long)g->M * shard / n_shards), p1 = (int)((long long)g->M * (shard + 1) / n_shards);
+  int xl1 = 0, xrows = 0;
+  const bool xmode = xc && (flags & FHTB_FAR) && x_supported(g, n_shards, &xl1, &xrows);
+  if (xmode) {
+    if (int r = run_exchange(g, ctx, rs, d_req, C, ldc, F, ldf, shard, n_shards, xl1, xrows, *xc, cv, st)) return r;
+  }
   if ((flags & FHTB_FAR) && !g->blocks.empty() && p1 > p0) {
     FarPlan fp;
-    plan_far(g, rs, fp);
+    plan_far(g, rs, fp, xmode ? 1 : 0);
     const long long nu = (long long)fp.units.size();
     if (nu > 0) {
       UnitDesc* d_units = cv.take<UnitDesc>(nu);
@@ -925,6 +1116,10 @@ int fhtb_apply_part(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req,
   }
   return FHTB_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 // --------------------------------------------------------------- direct
 namespace {

@@ -71,6 +71,14 @@ struct FarArgs {
   const double* w0_tab;         // omega_n^{-1/2}, n = 1..L (direct mode)
   const double* iw_tab;         // 1/omega_n
   int p0, p1;                   // pair range of this shard (direct: pairs p; chirp: terms 2p0 .. 2p1-1)
+  // distributed four-step (exchange mode, xw > 0 ranks): pass 1 covers the
+  // column slab n1 in [xn1, xn1 + L1/xw) and writes X[peer][unit][pair][j][n1 - xn1];
+  // pass 2 covers the column pairs c in [xc0, xc0 + gridDim.x) and reads the
+  // received X[src][unit][pair][j][n1 local]; xrow[k2] = (owner, j).
+  int xw, xlog, xrows, xc0;
+  long long xn1, xchunk;
+  const int2* xrow;
+  const double2* xin;
 };
 cudaError_t launch_col_tables(double* w0, double* iw, long long L, double gamma, cudaStream_t st);
 
@@ -87,6 +95,8 @@ constexpr int kNearRT = 64;
 cudaError_t launch_far_onepass(const FarArgs& a, int logN1, int n_units, cudaStream_t st);
 cudaError_t launch_far_pass1(const FarArgs& a, int logN2, int n_units, cudaStream_t st);
 cudaError_t launch_far_pass2(const FarArgs& a, int logN1, int n_units, cudaStream_t st);
+// exchange mode: pass 2 over n_pairs column pairs starting at a.xc0
+cudaError_t launch_far_pass2x_range(const FarArgs& a, int logN1, int n_pairs, int n_units, cudaStream_t st);
 cudaError_t launch_far_reduce(const FarArgs& a, int n_units, cudaStream_t st);
 cudaError_t launch_far_colgen(const FarArgs& a, int logN1, int n_units, cudaStream_t st);
 cudaError_t launch_far_rowdot(const FarArgs& a, int n_units, cudaStream_t st);

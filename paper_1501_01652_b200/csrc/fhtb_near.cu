@@ -32,12 +32,17 @@ constexpr int kNearThreads = 256;
 // JT: request columns per CTA (64, or 128 when a vector group needs more,
 // e.g. Fourier-Bessel and DHT batches -- the Bessel tile is then generated
 // once for all of them).
+// Shared-memory row strides are padded so that the m8n8k4 fp64 fragment
+// loads are bank-conflict free: A rows (8 rows x 4 doubles per fragment) by
+// 4 doubles, B rows (4 rows x 8 doubles) by 8 doubles.
 template <int NORD, int JT> struct NearCfg {
   static constexpr int NK = NORD <= 2 ? 16 : (NORD <= 4 ? 8 : 4);   // grid columns per step
   static constexpr int K = NK * NORD;                                // MMA depth per step
-  static constexpr int A_ELEMS = kRT * K;
-  static constexpr int B_ELEMS = K * JT;
-  static constexpr int C_ELEMS = kRT * JT;
+  static constexpr int KA = K + 4;                                   // As row stride
+  static constexpr int JB = JT + 8;                                  // Bs / Cs row stride
+  static constexpr int A_ELEMS = kRT * KA;
+  static constexpr int B_ELEMS = K * JB;
+  static constexpr int C_ELEMS = kRT * JB;
   static constexpr int SMEM = 8 * ((A_ELEMS + B_ELEMS) > C_ELEMS ? (A_ELEMS + B_ELEMS) : C_ELEMS);
 };
 
@@ -48,10 +53,10 @@ __device__ __forceinline__ double ipow(double x, int p) {
 }
 
 template <int NORD, int JT>
-__global__ void __launch_bounds__(kNearThreads)
+__global__ void __launch_bounds__(kNearThreads, 2)
 near_kernel(NearArgs a) {
   using Cfg = NearCfg<NORD, JT>;
-  constexpr int NK = Cfg::NK, K = Cfg::K;
+  constexpr int NK = Cfg::NK, K = Cfg::K, KA = Cfg::KA, JB = Cfg::JB;
   extern __shared__ double smem[];
   double* As = smem;                       // [kRT][K]
   double* Bs = smem + Cfg::A_ELEMS;        // [K][JT]
@@ -112,7 +117,7 @@ near_kernel(NearArgs a) {
         }
       }
 #pragma unroll
-      for (int u = 0; u < NORD; ++u) As[i * K + u * NK + q] = vals[u];
+      for (int u = 0; u < NORD; ++u) As[i * KA + u * NK + q] = vals[u];
     }
     // ---- weighted coefficient tile: Bs[u*NK + q][c] = w_c[u] * x_c[n]
     for (int e = tid; e < NK * JT; e += kNearThreads) {
@@ -129,19 +134,19 @@ near_kernel(NearArgs a) {
         }
       }
 #pragma unroll
-      for (int u = 0; u < NORD; ++u) Bs[(u * NK + q) * JT + c] = r ? r->w[u] * x : 0.0;
+      for (int u = 0; u < NORD; ++u) Bs[(u * NK + q) * JB + c] = r ? r->w[u] * x : 0.0;
     }
     __syncthreads();
     // ---- DMMA: warp w owns rows [8w, 8w+8)
 #pragma unroll
     for (int kk = 0; kk < K / 4; ++kk) {
       wmma::fragment<wmma::matrix_a, 8, 8, 4, double, wmma::row_major> fa;
-      wmma::load_matrix_sync(fa, As + (warp * 8) * K + kk * 4, K);
+      wmma::load_matrix_sync(fa, As + (warp * 8) * KA + kk * 4, KA);
 #pragma unroll
       for (int f = 0; f < JT / 8; ++f) {
         if (f < nfrag) {
           wmma::fragment<wmma::matrix_b, 8, 8, 4, double, wmma::row_major> fb;
-          wmma::load_matrix_sync(fb, Bs + (kk * 4) * JT + f * 8, JT);
+          wmma::load_matrix_sync(fb, Bs + (kk * 4) * JB + f * 8, JB);
           wmma::mma_sync(acc[f], fa, fb, acc[f]);
         }
       }
@@ -151,7 +156,7 @@ near_kernel(NearArgs a) {
   // ---- epilogue: reduce request columns into vectors with post factors
 #pragma unroll
   for (int f = 0; f < JT / 8; ++f)
-    wmma::store_matrix_sync(Cs + (warp * 8) * JT + f * 8, acc[f], JT, wmma::mem_row_major);
+    wmma::store_matrix_sync(Cs + (warp * 8) * JB + f * 8, acc[f], JB, wmma::mem_row_major);
   __syncthreads();
   const int v0 = a.grp_v0[g], v1 = a.grp_v0[g + 1];
   const int nv = v1 - v0;
@@ -165,7 +170,7 @@ near_kernel(NearArgs a) {
     for (int c = 0; c < nq; ++c) {
       const ReqDesc* r = a.reqs + q0 + c;
       if (r->vec != vec) continue;
-      double p = Cs[i * JT + c];
+      double p = Cs[i * JB + c];
       if (r->pr) p *= ipow((double)k / a.Ld, r->pr);
       if (r->post_e && r->pe) p *= ipow(r->post_e[j], r->pe);
       s += p;
@@ -208,7 +213,9 @@ static cudaError_t launch_near_j(const NearArgs& a, int n_tiles, int n_groups, c
   if (a.n_orders <= 1) return launch_near_t<1, JT>(a, n_tiles, n_groups, st);
   if (a.n_orders <= 2) return launch_near_t<2, JT>(a, n_tiles, n_groups, st);
   if (a.n_orders <= 4) return launch_near_t<4, JT>(a, n_tiles, n_groups, st);
+  if (a.n_orders <= 6) return launch_near_t<6, JT>(a, n_tiles, n_groups, st);
   if (a.n_orders <= 8) return launch_near_t<8, JT>(a, n_tiles, n_groups, st);
+  if (a.n_orders <= 12) return launch_near_t<12, JT>(a, n_tiles, n_groups, st);
   return launch_near_t<16, JT>(a, n_tiles, n_groups, st);
 }
 

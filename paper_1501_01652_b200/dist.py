@@ -54,16 +54,37 @@ def sharded_transform(fn, C, group=None, gather=True):
     return gather_rows(out, C.shape[0], group) if gather else out
 
 
-def distributed_transform(fn, *args, group=None, **kwargs):
+def all_to_all_exchange(group=None):
+    """The exchange callable of the distributed four-step: equal chunks of
+    the send buffer go to every rank (NCCL all-to-all over NVLink/NVSwitch on
+    the current stream)."""
+    def xfn(send, recv, bytes_per_peer):
+        world = dist.get_world_size(group)
+        m = world * bytes_per_peer
+        dist.all_to_all_single(recv[:m], send[:m], group=group)
+    return xfn
+
+
+def distributed_transform(fn, *args, group=None, exchange="pairs", **kwargs):
     """Evaluate ONE transform call fn(*args, **kwargs) (e.g.
     schlomilch_fast(params, c)) split across the ranks of `group`; every rank
     passes the same arguments and receives the full result (sum of the rank
     partials).  Pass CUDA tensors to keep the result on the device; a numpy
-    result is reduced through a tensor on the backend's device."""
+    result is reduced through a tensor on the backend's device.
+
+    exchange="pairs"    -- each rank computes a share of the term pairs of every
+                           block (no exchange before the final all-reduce);
+    exchange="alltoall" -- full blocks of power-of-two grids run as a
+                           distributed four-step FFT with one all-to-all per
+                           round (north star: the FFT transpose over NVLink);
+                           other work as "pairs"."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return fn(*args, **kwargs)
+    if exchange not in ("pairs", "alltoall"):
+        raise ValueError("exchange must be 'pairs' or 'alltoall'")
     world, rank = dist.get_world_size(group), dist.get_rank(group)
-    with _device.sharding(rank, world):
+    xfn = all_to_all_exchange(group) if exchange == "alltoall" else None
+    with _device.sharding(rank, world, exchange=xfn):
         out = fn(*args, **kwargs)
     if isinstance(out, torch.Tensor):
         dist.all_reduce(out, group=group)

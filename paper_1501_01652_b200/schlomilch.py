@@ -174,13 +174,48 @@ class _Grid:
         if not requests:
             return F
         arr, keep = _pack_requests(requests)
+        s, n = _device.shard()
+        xfn = _device.shard_exchange()
+        unit = self._lib.fhtb_apply_x_unit_bytes(self.handle, n) if (xfn is not None and n > 1) else 0
+        if unit:
+            return self._apply_exchange(arr, len(requests), C, F, flags, s, n, xfn, unit, keep)
         ws_n = self._lib.fhtb_apply_workspace(self.handle, len(requests), C.shape[0], flags)
         ws = _device.workspace(ws_n)
-        s, n = _device.shard()
         _lib.check(self._lib.fhtb_apply_part(self.handle, arr, len(requests), _device.ptr(C), C.stride(0),
                                              C.shape[0], _device.ptr(F), F.stride(0), flags, s, n,
                                              _device.ptr(ws), ws.numel(), _device.stream_ptr()))
         del keep
+        return F
+
+    X_BUDGET = 1 << 30          # bytes per exchange buffer (send; recv the same)
+
+    def _apply_exchange(self, arr, n_req, C, F, flags, s, n, xfn, unit, keep):
+        """fhtb_apply_x: the all-to-all between pass 1 and pass 2 is xfn."""
+        xbytes = max(1, self.X_BUDGET // unit) * unit
+        dev = C.device
+        send = torch.empty(xbytes, dtype=torch.uint8, device=dev)
+        recv = torch.empty(xbytes, dtype=torch.uint8, device=dev)
+        errors = []
+
+        def _cb(user, rnd, bpp):
+            try:
+                xfn(send, recv, int(bpp))
+                return 0
+            except Exception as exc:          # surfaced after the library returns
+                errors.append(exc)
+                return 1
+
+        cb = _lib.EXCHANGE_FN(_cb)
+        ws_n = self._lib.fhtb_apply_x_workspace(self.handle, n_req, C.shape[0], flags, n, xbytes)
+        ws = torch.empty(max(int(ws_n), 256), dtype=torch.uint8, device=dev)
+        code = self._lib.fhtb_apply_x(self.handle, arr, n_req, _device.ptr(C), C.stride(0), C.shape[0],
+                                      _device.ptr(F), F.stride(0), flags, s, n, _device.ptr(send),
+                                      _device.ptr(recv), xbytes, cb, None, _device.ptr(ws), ws.numel(),
+                                      _device.stream_ptr())
+        if errors:
+            raise errors[0]
+        _lib.check(code)
+        del keep, cb
         return F
 
 

@@ -80,3 +80,98 @@ def test_distributed_transform_single_process(cuda_dev):
     c = torch.from_numpy(np.random.default_rng(1).standard_normal(4096)).to(cuda_dev)
     params = fh.select_params(0, 4096, 1e-8)
     assert torch.equal(distributed_transform(fh.schlomilch_fast, params, c), fh.schlomilch_fast(params, c))
+
+
+# ------------------------------------------- distributed four-step (exchange)
+def _exchange_split(fn, world, budget=None):
+    """Run `world` simulated ranks as threads on the one GPU (own stream
+    each); their exchange callbacks implement the all-to-all by copies between
+    the ranks' buffers, bracketed by barriers.  Returns the rank outputs and
+    the number of exchange rounds seen by each rank."""
+    import threading
+
+    from paper_1501_01652_b200.schlomilch import _Grid
+
+    barrier = threading.Barrier(world)
+    sends, outs, rounds, errs = {}, {}, {r: 0 for r in range(world)}, []
+    old_budget = _Grid.X_BUDGET
+    if budget is not None:
+        _Grid.X_BUDGET = budget
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                def xfn(send, recv, bpp):
+                    st.synchronize()
+                    sends[r] = send
+                    barrier.wait()
+                    for s in range(world):
+                        recv[s * bpp:(s + 1) * bpp].copy_(sends[s][r * bpp:(r + 1) * bpp])
+                    st.synchronize()
+                    rounds[r] += 1
+                    barrier.wait()
+
+                with _device.sharding(r, world, exchange=xfn):
+                    out = fn()
+                st.synchronize()
+                outs[r] = out.clone()
+        except Exception as exc:                         # pragma: no cover - reported below
+            errs.append(exc)
+            barrier.abort()
+
+    ths = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    try:
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join(300)
+    finally:
+        _Grid.X_BUDGET = old_budget
+    if errs:
+        raise errs[0]
+    return [outs[r] for r in range(world)], rounds
+
+
+@pytest.mark.parametrize("n,nu,gamma,world", [(2 ** 14, 0, 0.0, 2), (2 ** 14, 4, 4.0, 4), (2 ** 16, 4, 4.0, 8)])
+def test_alltoall_four_step_sums_to_full(cuda_dev, n, nu, gamma, world):
+    rng = np.random.default_rng([8, n, world])
+    C = torch.from_numpy(rng.standard_normal((3, n)) / np.arange(1, n + 1)).to(cuda_dev)
+    params = fh.select_params(nu, n, 1e-15, gamma=gamma)
+    fn = lambda: fh.schlomilch_fast(params, C)
+    full = fn()
+    from paper_1501_01652_b200.schlomilch import _grid
+    sc = fh.build_partition(params)
+    g = _grid(params.n, params.gamma, params.m_terms, sc.blocks, sc.mask_segments, [nu])
+    unit = g._lib.fhtb_apply_x_unit_bytes(g.handle, world)
+    assert unit > 0                                      # the exchange path is taken
+    outs, rounds = _exchange_split(fn, world, budget=unit)   # one unit per round
+    assert all(v == rounds[0] and v >= 3 for v in rounds.values())
+    tot = torch.stack(outs).sum(0)
+    l1 = float(C.abs().sum(1).max())
+    assert float((tot - full).abs().max()) <= 2e-15 * l1
+
+
+def test_alltoall_default_budget_single_round(cuda_dev):
+    n = 2 ** 15
+    C = torch.from_numpy(np.random.default_rng(3).standard_normal((2, n))).to(cuda_dev)
+    params = fh.select_params(0, n, 1e-8)
+    fn = lambda: fh.schlomilch_fast(params, C)
+    full = fn()
+    outs, rounds = _exchange_split(fn, 2)
+    assert rounds == {0: 1, 1: 1}
+    tot = outs[0] + outs[1]
+    assert float((tot - full).abs().max()) <= 2e-15 * float(C.abs().sum(1).max())
+
+
+def test_alltoall_falls_back_without_full_blocks(cuda_dev):
+    # chirp-z grid (non-power-of-two N): no exchange rounds, pair split
+    n = 3000
+    C = torch.from_numpy(np.random.default_rng(5).standard_normal(n)).to(cuda_dev)
+    params = fh.select_params(0, n, 1e-15)
+    fn = lambda: fh.schlomilch_fast(params, C)
+    full = fn()
+    outs, rounds = _exchange_split(fn, 3)
+    assert rounds == {0: 0, 1: 0, 2: 0}
+    assert _close(outs[0] + outs[1] + outs[2], full, C.cpu().numpy())
