@@ -136,3 +136,36 @@ def test_sharding_context_validation():
             assert _device.shard() == (0, 2)
         assert _device.shard() == (1, 3)
     assert _device.shard() == (0, 1)
+
+
+def _a2a_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1501_01652_b200.dist import all_to_all_exchange
+
+        bpp = 24
+        send = torch.zeros(world * bpp + 16, dtype=torch.uint8)    # buffers may be larger than used
+        for s in range(world):
+            send[s * bpp:(s + 1) * bpp] = 10 * rank + s
+        recv = torch.full((world * bpp + 16,), 255, dtype=torch.uint8)
+        all_to_all_exchange()(send, recv, bpp)
+        ok = all(bool((recv[s * bpp:(s + 1) * bpp] == 10 * s + rank).all()) for s in range(world))
+        ok = ok and bool((recv[world * bpp:] == 255).all())
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_all_to_all_exchange():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_a2a_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    res = dict(q.get(timeout=10) for _ in range(2))
+    assert res == {0: True, 1: True}
