@@ -732,7 +732,7 @@ static cudaError_t p1_t(const FarArgs& a, int n_units, cudaStream_t st) {
   const int smem = (W * (N2 + PAD) + W * N2) * 16;   // FFT buffers (staging) + four-step twiddles
   CUtensorMap m;
   std::memset(&m, 0, sizeof m);
-  const bool tma = W >= 2 && !a.xw && !(g_far_variant & 0x10000) && g_tmap(&m, a, n_units, W, N2 < 256 ? N2 : 256);
+  const bool tma = !a.xw && !(g_far_variant & 0x10000) && g_tmap(&m, a, n_units, W, N2 < 256 ? N2 : 256);
   auto k = tma ? far_pass1_kernel<N2, E, W, MINB, true> : far_pass1_kernel<N2, E, W, MINB, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -745,6 +745,8 @@ static cudaError_t p1_t(const FarArgs& a, int n_units, cudaStream_t st) {
 template <int N2>
 static cudaError_t p1_d(const FarArgs& a, int n_units, cudaStream_t st) {
   constexpr int E = N2 >= 16 ? 16 : N2;
+  // 512-point columns: 128-thread CTAs, 3 per SM (as the tuned 1024 shape)
+  if (N2 == 512) return p1_t<N2, E, 4, 3>(a, n_units, st);
   constexpr int W = N2 >= 4096 ? 1 : 4096 / N2;
   return p1_t<N2, E, W, 1>(a, n_units, st);
 }
@@ -775,6 +777,7 @@ static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
   constexpr int E = MODE == 2 ? (N1 >= 8 ? 8 : N1) : (N1 >= 16 ? 16 : N1);
   // two columns of 2048 with E = 16: 256 threads, 2 CTAs/SM measured best
   constexpr int MINB = ((MODE == 0 || MODE == 3) && N1 == 2048) ? 2
+                       : ((MODE == 0 || MODE == 3) && N1 == 1024) ? 3
                        : (MODE == 2 && N1 <= 1024) ? (N1 <= 512 ? 4 : 2) : 1;
   return p2_t<N1, E, MODE, MINB>(a, gx, gy, st);
 }
