@@ -32,6 +32,7 @@ thread_local std::string g_err;
 int64_t g_far_chunk_bytes = 1LL << 30;     // two-pass intermediate budget
 int64_t g_near_chunk_cols = 8192;          // near-field column chunk per tile
 int g_far_prune = 1;                       // pruned side blocks (direct two-pass)
+int g_near_split = 1;                      // near field: order-parity classes
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -253,6 +254,65 @@ int make_groups(const std::vector<ReqDesc>& sorted, int n_vec, std::vector<int>&
   return FHTB_OK;
 }
 
+// Near-field request layout with order-parity classes (universe {0..n-1},
+// n >= 3): per group of whole vectors, requests whose weights touch only even
+// orders first, then only odd, then mixed; the first two classes are padded to
+// a multiple of 8 columns with inert requests (zero weights, vec -1, no
+// columns), so that every 8-column MMA fragment has one class.
+int make_groups_split(const std::vector<ReqDesc>& sorted, int n_vec, int n_orders, std::vector<ReqDesc>& out,
+                      std::vector<int>& q0, std::vector<int>& v0, std::vector<int2>& cls, int* max_cols) {
+  out.clear();
+  q0.clear();
+  v0.clear();
+  cls.clear();
+  *max_cols = 0;
+  auto klass = [&](const ReqDesc& r) {
+    bool ev = false, od = false;
+    for (int u = 0; u < n_orders; ++u)
+      if (r.w[u] != 0.0) ((u & 1) ? od : ev) = true;
+    return (ev && od) ? 2 : (od ? 1 : 0);
+  };
+  std::vector<std::vector<int>> byvec(n_vec);
+  for (int i = 0; i < (int)sorted.size(); ++i) byvec[sorted[i].vec].push_back(i);
+  ReqDesc inert;
+  std::memset(&inert, 0, sizeof inert);
+  inert.vec = -1;
+  inert.col_lo = (long long)1 << 62;
+  auto padded = [](int n) { return (n + 7) & ~7; };
+  int v = 0;
+  while (v < n_vec) {
+    int cnt[3] = {0, 0, 0};
+    int v1 = v;
+    while (v1 < n_vec) {
+      int c2[3] = {cnt[0], cnt[1], cnt[2]};
+      for (int i : byvec[v1]) c2[klass(sorted[i])]++;
+      if (padded(c2[0]) + padded(c2[1]) + c2[2] > kNearMaxCols) break;
+      for (int k = 0; k < 3; ++k) cnt[k] = c2[k];
+      ++v1;
+    }
+    if (v1 == v) return fail(FHTB_EINVAL, "too many requests for one vector");
+    q0.push_back((int)out.size());
+    v0.push_back(v);
+    const int base = (int)out.size();
+    for (int k = 0; k < 3; ++k) {
+      for (int vv = v; vv < v1; ++vv)
+        for (int i : byvec[vv])
+          if (klass(sorted[i]) == k) out.push_back(sorted[i]);
+      if (k < 2)
+        while ((int)out.size() - base < padded((k == 0 ? 0 : padded(cnt[0])) + cnt[k]) ||
+               ((int)out.size() - base) % 8)
+          out.push_back(inert);
+      if (k == 0) cls.push_back(make_int2((int)out.size() - base, 0));
+      if (k == 1) cls.back().y = (int)out.size() - base;
+    }
+    *max_cols = std::max(*max_cols, (int)out.size() - base);
+    v = v1;
+  }
+  q0.push_back((int)out.size());
+  v0.push_back(v);
+  return FHTB_OK;
+}
+
 // Near tiles over a list of segments (r0, r1, c_end) in grid index space.
 void make_tiles(const std::vector<long long>& segs, long long first, long long stride, long long n_data_cols,
                 long long n_out, std::vector<NearTile>& tiles, std::vector<NearRowTile>& rts, long long& n_slots) {
@@ -372,6 +432,10 @@ int fhtb_set_option(const char* key, int64_t value) {
   if (!key) return fail(FHTB_EINVAL, "null key");
   if (!std::strcmp(key, "far_prune")) {
     g_far_prune = (int)value;
+    return FHTB_OK;
+  }
+  if (!std::strcmp(key, "near_split")) {
+    g_near_split = value ? 1 : 0;
     return FHTB_OK;
   }
   if (!std::strcmp(key, "chirp_variant")) {
@@ -745,7 +809,12 @@ size_t ws_need(const fhtb_grid* g, int n_req, int n_vec, int flags) {
   size_t s = align_up(sizeof(ReqDesc) * std::max(n_req, 1));
   if (flags & FHTB_FAR) s += far_ws(g, n_req);
   s += 2 * align_up(sizeof(int) * (n_vec + 2));
-  if (flags & FHTB_NEAR) s += align_up(sizeof(double) * (size_t)g->n_slots * n_vec * kNearRT);
+  if (flags & FHTB_NEAR) {
+    s += align_up(sizeof(double) * (size_t)g->n_slots * n_vec * kNearRT);
+    // parity-class layout: a padded copy of the requests (<= 16 inert per vector) + class ends
+    s += align_up(sizeof(ReqDesc) * ((size_t)std::max(n_req, 1) + 16 * (size_t)n_vec));
+    s += align_up(sizeof(int2) * (n_vec + 2));
+  }
   return s + 4096;
 }
 
@@ -1071,14 +1140,29 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
 
   if ((flags & FHTB_NEAR) && !g->tiles.empty()) {
     std::vector<int> q0, v0;
+    std::vector<int2> cls;
+    std::vector<ReqDesc> nreq;
     int max_cols = 0;
-    if (int r = make_groups(rs, n_vec, q0, v0, &max_cols)) return r;
+    bool identity = true;
+    for (int i = 0; i < (int)g->orders.size(); ++i) identity = identity && g->orders[i] == i;
+    const bool split = identity && g->orders.size() >= 3 && g_near_split;
+    if (split) {
+      if (int r = make_groups_split(rs, n_vec, (int)g->orders.size(), nreq, q0, v0, cls, &max_cols)) return r;
+    } else {
+      if (int r = make_groups(rs, n_vec, q0, v0, &max_cols)) return r;
+    }
     int* d_q0 = cv.take<int>(q0.size());
     int* d_v0 = cv.take<int>(v0.size());
+    int2* d_cls = split ? cv.take<int2>(cls.size()) : nullptr;
+    ReqDesc* d_nreq = split ? cv.take<ReqDesc>(nreq.size()) : nullptr;
     double* part = g->n_slots ? cv.take<double>((size_t)g->n_slots * n_vec * kNearRT) : nullptr;
     if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small");
     CU(cudaMemcpyAsync(d_q0, q0.data(), q0.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(d_v0, v0.data(), v0.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (split) {
+      CU(cudaMemcpyAsync(d_cls, cls.data(), cls.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+      CU(cudaMemcpyAsync(d_nreq, nreq.data(), nreq.size() * sizeof(ReqDesc), cudaMemcpyHostToDevice, st));
+    }
     NearArgs na;
     std::memset(&na, 0, sizeof na);
     na.tiles = g->d_tiles;
@@ -1098,9 +1182,10 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
       if (g->orders[i] != i) na.orders_identity = 0;
     }
     na.jtab = ctx->jtab;
-    na.reqs = d_req;
+    na.reqs = split ? d_nreq : d_req;
     na.grp_q0 = d_q0;
     na.grp_v0 = d_v0;
+    na.grp_cls = d_cls;
     na.C = C;
     na.ldc = ldc;
     na.n_data_cols = g->n_data_cols;

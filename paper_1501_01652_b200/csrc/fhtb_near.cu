@@ -66,6 +66,18 @@ near_kernel(NearArgs a) {
   const int g = blockIdx.y;
   const int q0 = a.grp_q0[g], q1 = a.grp_q0[g + 1];
   const int nq = q1 - q0;
+  // order-parity classes (universe {0..n-1}): the group's columns are
+  // [0, fe*8) requests of even orders only, [fe*8, fo*8) odd orders only,
+  // then mixed.  The K dimension is laid out even orders first (PE of them),
+  // so each class contracts only its half of K.
+  constexpr int PE = (NORD + 1) / 2;
+  const bool split = a.grp_cls != nullptr;
+  int fe = 0, fo = 0;
+  if (split) {
+    const int2 cl = a.grp_cls[g];
+    fe = cl.x >> 3;
+    fo = cl.y >> 3;
+  }
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   if (a.n_shards > 1 && (int)(blockIdx.x % a.n_shards) != a.shard) {
@@ -117,7 +129,10 @@ near_kernel(NearArgs a) {
         }
       }
 #pragma unroll
-      for (int u = 0; u < NORD; ++u) As[i * KA + u * NK + q] = vals[u];
+      for (int u = 0; u < NORD; ++u) {
+        const int pu = split ? ((u & 1) ? PE + (u >> 1) : (u >> 1)) : u;
+        As[i * KA + pu * NK + q] = vals[u];
+      }
     }
     // ---- weighted coefficient tile: Bs[u*NK + q][c] = w_c[u] * x_c[n]
     for (int e = tid; e < NK * JT; e += kNearThreads) {
@@ -134,17 +149,23 @@ near_kernel(NearArgs a) {
         }
       }
 #pragma unroll
-      for (int u = 0; u < NORD; ++u) Bs[(u * NK + q) * JB + c] = r ? r->w[u] * x : 0.0;
+      for (int u = 0; u < NORD; ++u) {
+        const int pu = split ? ((u & 1) ? PE + (u >> 1) : (u >> 1)) : u;
+        Bs[(pu * NK + q) * JB + c] = r ? r->w[u] * x : 0.0;
+      }
     }
     __syncthreads();
-    // ---- DMMA: warp w owns rows [8w, 8w+8)
+    // ---- DMMA: warp w owns rows [8w, 8w+8).  Fragment f of class 0 (even
+    // orders) contracts only k-steps < KE, class 1 (odd) only >= KE.
+    constexpr int KE = (PE * NK) / 4;     // k-steps of the even-order half
 #pragma unroll
     for (int kk = 0; kk < K / 4; ++kk) {
       wmma::fragment<wmma::matrix_a, 8, 8, 4, double, wmma::row_major> fa;
       wmma::load_matrix_sync(fa, As + (warp * 8) * KA + kk * 4, KA);
 #pragma unroll
       for (int f = 0; f < JT / 8; ++f) {
-        if (f < nfrag) {
+        const bool on = f < nfrag && (kk < KE ? f < fe || f >= fo : f >= fe);
+        if (on) {
           wmma::fragment<wmma::matrix_b, 8, 8, 4, double, wmma::row_major> fb;
           wmma::load_matrix_sync(fb, Bs + (kk * 4) * JB + f * 8, JB);
           wmma::mma_sync(acc[f], fa, fb, acc[f]);
