@@ -313,6 +313,24 @@ int make_groups_split(const std::vector<ReqDesc>& sorted, int n_vec, int n_order
   return FHTB_OK;
 }
 
+// Group-local columns of every vector's requests, in column order (the
+// near-field epilogue sums exactly those, in that order).
+void vec_columns(const std::vector<ReqDesc>& reqs, const std::vector<int>& q0, int n_vec, std::vector<int>& vstart,
+                 std::vector<int>& vcol) {
+  std::vector<std::vector<int>> by(n_vec);
+  for (int g = 0; g + 1 < (int)q0.size(); ++g)
+    for (int q = q0[g]; q < q0[g + 1]; ++q)
+      if (reqs[q].vec >= 0) by[reqs[q].vec].push_back(q - q0[g]);
+  vstart.assign(n_vec + 1, 0);
+  vcol.clear();
+  for (int v = 0; v < n_vec; ++v) {
+    vstart[v] = (int)vcol.size();
+    vcol.insert(vcol.end(), by[v].begin(), by[v].end());
+  }
+  vstart[n_vec] = (int)vcol.size();
+  if (vcol.empty()) vcol.push_back(0);
+}
+
 // Near tiles over a list of segments (r0, r1, c_end) in grid index space.
 void make_tiles(const std::vector<long long>& segs, long long first, long long stride, long long n_data_cols,
                 long long n_out, std::vector<NearTile>& tiles, std::vector<NearRowTile>& rts, long long& n_slots) {
@@ -814,6 +832,7 @@ size_t ws_need(const fhtb_grid* g, int n_req, int n_vec, int flags) {
     // parity-class layout: a padded copy of the requests (<= 16 inert per vector) + class ends
     s += align_up(sizeof(ReqDesc) * ((size_t)std::max(n_req, 1) + 16 * (size_t)n_vec));
     s += align_up(sizeof(int2) * (n_vec + 2));
+    s += align_up(sizeof(int) * (n_vec + 2)) + align_up(sizeof(int) * ((size_t)n_req + 2));
   }
   return s + 4096;
 }
@@ -1151,14 +1170,20 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
     } else {
       if (int r = make_groups(rs, n_vec, q0, v0, &max_cols)) return r;
     }
+    std::vector<int> vstart, vcol;
+    vec_columns(split ? nreq : rs, q0, n_vec, vstart, vcol);
     int* d_q0 = cv.take<int>(q0.size());
     int* d_v0 = cv.take<int>(v0.size());
+    int* d_vs = cv.take<int>(vstart.size());
+    int* d_vc = cv.take<int>(vcol.size());
     int2* d_cls = split ? cv.take<int2>(cls.size()) : nullptr;
     ReqDesc* d_nreq = split ? cv.take<ReqDesc>(nreq.size()) : nullptr;
     double* part = g->n_slots ? cv.take<double>((size_t)g->n_slots * n_vec * kNearRT) : nullptr;
     if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small");
     CU(cudaMemcpyAsync(d_q0, q0.data(), q0.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(d_v0, v0.data(), v0.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(d_vs, vstart.data(), vstart.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(d_vc, vcol.data(), vcol.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     if (split) {
       CU(cudaMemcpyAsync(d_cls, cls.data(), cls.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
       CU(cudaMemcpyAsync(d_nreq, nreq.data(), nreq.size() * sizeof(ReqDesc), cudaMemcpyHostToDevice, st));
@@ -1186,6 +1211,8 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
     na.grp_q0 = d_q0;
     na.grp_v0 = d_v0;
     na.grp_cls = d_cls;
+    na.vstart = d_vs;
+    na.vcol = d_vc;
     na.C = C;
     na.ldc = ldc;
     na.n_data_cols = g->n_data_cols;
@@ -1225,6 +1252,7 @@ size_t fhtb_direct_workspace(const fhtb_direct_desc* d, int32_t n_req, int32_t n
   s += align_up(sizeof(NearTile) * std::max<size_t>(tiles.size(), 1));
   s += align_up(sizeof(NearRowTile) * std::max<size_t>(rts.size(), 1));
   s += 2 * align_up(sizeof(int) * (n_vec + 2));
+  s += align_up(sizeof(int) * (n_vec + 2)) + align_up(sizeof(int) * ((size_t)n_req + 2));
   s += align_up(sizeof(double) * (size_t)ns * n_vec * kNearRT);
   return s + 4096;
 }
@@ -1260,11 +1288,17 @@ int fhtb_direct_apply(const fhtb_direct_desc* d, const fhtb_request* reqs, int32
   ReqDesc* d_req = cv.take<ReqDesc>(n_req);
   NearTile* d_tiles = cv.take<NearTile>(std::max<size_t>(tiles.size(), 1));
   NearRowTile* d_rts = cv.take<NearRowTile>(std::max<size_t>(rts.size(), 1));
+  std::vector<int> vstart, vcol;
+  vec_columns(rs, q0, n_vec, vstart, vcol);
   int* d_q0 = cv.take<int>(q0.size());
   int* d_v0 = cv.take<int>(v0.size());
+  int* d_vs = cv.take<int>(vstart.size());
+  int* d_vc = cv.take<int>(vcol.size());
   double* part = ns ? cv.take<double>((size_t)ns * n_vec * kNearRT) : nullptr;
   if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small");
   CU(cudaMemcpyAsync(d_req, rs.data(), n_req * sizeof(ReqDesc), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_vs, vstart.data(), vstart.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_vc, vcol.data(), vcol.size() * sizeof(int), cudaMemcpyHostToDevice, st));
   if (!tiles.empty()) CU(cudaMemcpyAsync(d_tiles, tiles.data(), tiles.size() * sizeof(NearTile), cudaMemcpyHostToDevice, st));
   if (!rts.empty()) CU(cudaMemcpyAsync(d_rts, rts.data(), rts.size() * sizeof(NearRowTile), cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(d_q0, q0.data(), q0.size() * sizeof(int), cudaMemcpyHostToDevice, st));
@@ -1288,6 +1322,8 @@ int fhtb_direct_apply(const fhtb_direct_desc* d, const fhtb_request* reqs, int32
   na.reqs = d_req;
   na.grp_q0 = d_q0;
   na.grp_v0 = d_v0;
+  na.vstart = d_vs;
+  na.vcol = d_vc;
   na.C = C;
   na.ldc = ldc;
   na.n_data_cols = std::min(d->n_data_cols, d->n_cols);

@@ -33,6 +33,8 @@ struct NearArgs {
   const int* grp_q0;            // requests of group g: [grp_q0[g], grp_q0[g+1])
   const int* grp_v0;            // vectors of group g
   const int2* grp_cls;          // per group: end columns of the even / odd order classes (or null)
+  const int* vstart;            // columns of vector v: vcol[vstart[v] .. vstart[v+1]) (group-local)
+  const int* vcol;
   const double* C;
   long long ldc, n_data_cols;
   double* F;

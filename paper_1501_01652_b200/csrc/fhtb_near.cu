@@ -188,9 +188,9 @@ near_kernel(NearArgs a) {
     const long long j = tile.j0 + i;
     const long long k = a.first + a.stride * j;
     double s = 0.0;
-    for (int c = 0; c < nq; ++c) {
+    for (int idx = a.vstart[vec]; idx < a.vstart[vec + 1]; ++idx) {
+      const int c = a.vcol[idx];
       const ReqDesc* r = a.reqs + q0 + c;
-      if (r->vec != vec) continue;
       double p = Cs[i * JB + c];
       if (r->pr) p *= ipow((double)k / a.Ld, r->pr);
       if (r->post_e && r->pe) p *= ipow(r->post_e[j], r->pe);
