@@ -118,83 +118,6 @@ __device__ __forceinline__ double jn(int nu, double z, const JOrder& c) {
   return jn_miller(nu, z);
 }
 
-// J_nu at NL arguments with the same dispatch as jn(); the Miller-range
-// arguments run ONE interleaved backward recurrence started at the largest
-// start order among them (as the reference starts a whole tile at the
-// tile maximum, bessel.py:206-207), so the NL independent chains hide the
-// fp64 latency of each other.
-template <int NL>
-__device__ __forceinline__ void jn_multi(int nu, const double (&z)[NL], const JOrder& c, double (&out)[NL]) {
-  bool mil[NL];
-  int k0 = -1;
-#pragma unroll
-  for (int l = 0; l < NL; ++l) {
-    mil[l] = false;
-    if (z[l] <= c.tlo) {
-      out[l] = jn_taylor(nu, z[l], c);
-    } else if (z[l] >= c.shi) {
-      out[l] = jn_hankel(z[l], c);
-    } else {
-      mil[l] = true;
-      out[l] = 0.0;
-      k0 = max(k0, miller_start(fmax((double)nu, z[l])));
-    }
-  }
-  if (k0 < 0) return;
-  double rz2[NL], up[NL], cur[NL], nrm[NL], cap[NL];
-#pragma unroll
-  for (int l = 0; l < NL; ++l) {
-    rz2[l] = mil[l] ? 2.0 / z[l] : 0.0;
-    up[l] = 0.0;
-    cur[l] = 1e-30;
-    nrm[l] = 0.0;
-    cap[l] = 0.0;
-  }
-  int k = k0;
-  if ((k - nu - 1) & 1) {
-#pragma unroll
-    for (int l = 0; l < NL; ++l) {
-      const double lo = fma((double)k * rz2[l], cur[l], -up[l]);
-      up[l] = cur[l];
-      cur[l] = lo;
-      if (((k - 1) & 1) == 0) nrm[l] += 2.0 * cur[l];
-    }
-    --k;
-  }
-  for (; k > nu + 1; k -= 2) {
-    const double kd = (double)k, kd1 = (double)(k - 1);
-    const bool even1 = ((k - 1) & 1) == 0;
-#pragma unroll
-    for (int l = 0; l < NL; ++l) {
-      const double lo = fma(kd * rz2[l], cur[l], -up[l]);
-      const double lo2 = fma(kd1 * rz2[l], lo, -cur[l]);
-      nrm[l] += 2.0 * (even1 ? lo : lo2);
-      up[l] = lo;
-      cur[l] = lo2;
-      if (fabs(cur[l]) > 1e250) {
-        cur[l] *= 1e-250; up[l] *= 1e-250; nrm[l] *= 1e-250;
-      }
-    }
-  }
-  for (; k > 0; --k) {
-    const int o = k - 1;
-#pragma unroll
-    for (int l = 0; l < NL; ++l) {
-      const double lo = fma((double)k * rz2[l], cur[l], -up[l]);
-      up[l] = cur[l];
-      cur[l] = lo;
-      if (o == nu) cap[l] = cur[l];
-      if ((o & 1) == 0) nrm[l] += (o == 0) ? cur[l] : 2.0 * cur[l];
-      if (fabs(cur[l]) > 1e250) {
-        cur[l] *= 1e-250; up[l] *= 1e-250; nrm[l] *= 1e-250; cap[l] *= 1e-250;
-      }
-    }
-  }
-#pragma unroll
-  for (int l = 0; l < NL; ++l)
-    if (mil[l]) out[l] = cap[l] / nrm[l];
-}
-
 // J_0..J_{omax}(z) into out[] (omax < OMAX).  Branch per element: Taylor is
 // not needed (Miller is accurate for all small z > 0); Hankel per order
 // where z clears that order's cutoff, sharing one sincos.
