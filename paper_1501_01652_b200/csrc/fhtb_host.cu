@@ -33,6 +33,7 @@ int64_t g_far_chunk_bytes = 1LL << 30;     // two-pass intermediate budget
 int64_t g_near_chunk_cols = 8192;          // near-field column chunk per tile
 int g_far_prune = 1;                       // pruned side blocks (direct two-pass)
 int g_near_split = 1;                      // near field: order-parity classes
+int g_far_streams = 2;                     // far-field chunks in flight (direct two-pass)
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -113,6 +114,35 @@ inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
 
 std::mutex g_mu;
 std::map<int, DevCtx> g_ctx;
+
+// Two auxiliary streams + events per (device, caller stream): far-field
+// chunks are computed on them two at a time and reduced in chunk order on the
+// caller's stream.
+struct AuxStreams {
+  cudaStream_t cs[2];
+  cudaEvent_t start, done[2], red[2];
+};
+std::map<std::pair<int, cudaStream_t>, AuxStreams> g_aux;
+
+int get_aux(cudaStream_t caller, AuxStreams** out) {
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_pair(dev, caller);
+  auto it = g_aux.find(key);
+  if (it == g_aux.end()) {
+    AuxStreams a;
+    for (int i = 0; i < 2; ++i) {
+      CU(cudaStreamCreateWithFlags(&a.cs[i], cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&a.done[i], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&a.red[i], cudaEventDisableTiming));
+    }
+    CU(cudaEventCreateWithFlags(&a.start, cudaEventDisableTiming));
+    it = g_aux.emplace(key, a).first;
+  }
+  *out = &it->second;
+  return FHTB_OK;
+}
 
 int get_ctx(DevCtx** out) {
   int dev = 0;
@@ -450,6 +480,11 @@ int fhtb_set_option(const char* key, int64_t value) {
   if (!key) return fail(FHTB_EINVAL, "null key");
   if (!std::strcmp(key, "far_prune")) {
     g_far_prune = (int)value;
+    return FHTB_OK;
+  }
+  if (!std::strcmp(key, "far_streams")) {
+    if (value < 1 || value > 2) return fail(FHTB_EINVAL, "far_streams must be 1 or 2");
+    g_far_streams = (int)value;
     return FHTB_OK;
   }
   if (!std::strcmp(key, "near_split")) {
@@ -819,7 +854,8 @@ size_t far_ws(const fhtb_grid* g, int n_req) {
   plan_far(g, rs, fp);
   size_t s = align_up(sizeof(UnitDesc) * std::max<size_t>(fp.units.size(), 1));
   s += align_up(sizeof(int2) * (fp.chunks.size() + 1));
-  s += align_up(fp.g_bytes) + align_up(fp.part_bytes);
+  const int nbuf = (g->direct && g->logN2 > 0) ? 2 : 1;     // chunks in flight
+  s += nbuf * (align_up(fp.g_bytes) + align_up(fp.part_bytes));
   return s;
 }
 
@@ -1076,7 +1112,15 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
       int2* d_ch = cv.take<int2>(fp.chunks.size());
       double2* G = fp.g_bytes ? (double2*)cv.take<char>(fp.g_bytes) : nullptr;
       double* part = fp.part_bytes ? (double*)cv.take<char>(fp.part_bytes) : nullptr;
+      // second buffer set: two chunks in flight on two streams (direct two-pass)
+      const bool pipe = g->direct && g->logN2 > 0 && g_far_streams > 1 && fp.chunks.size() > 1;
+      double2* G2 = (pipe && fp.g_bytes) ? (double2*)cv.take<char>(fp.g_bytes) : nullptr;
+      double* part2 = (pipe && fp.part_bytes) ? (double*)cv.take<char>(fp.part_bytes) : nullptr;
       if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small");
+      AuxStreams* ax = nullptr;
+      if (pipe) {
+        if (int r = get_aux(st, &ax)) return r;
+      }
       CU(cudaMemcpyAsync(d_units, fp.units.data(), nu * sizeof(UnitDesc), cudaMemcpyHostToDevice, st));
       CU(cudaMemcpyAsync(d_ch, fp.chunks.data(), fp.chunks.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
       FarArgs a;
@@ -1115,6 +1159,11 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
         CU(launch_far_onepass(a, g->logN1, (int)nu, st));
         CU(launch_far_reduce(a, (int)nu, st));
       } else {
+        if (pipe) {
+          // the aux streams start after the caller's prior work (C, F ready)
+          CU(cudaEventRecord(ax->start, st));
+          for (int b = 0; b < 2; ++b) CU(cudaStreamWaitEvent(ax->cs[b], ax->start, 0));
+        }
         for (size_t ci = 0; ci < fp.chunks.size(); ++ci) {
           const int lq = fp.chunk_logq[ci];
           const int n_units = fp.chunks[ci].y - fp.chunks[ci].x;
@@ -1131,16 +1180,33 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
             a.L1 = 1 << l1;
             a.L2 = 1 << l2;
             a.vranges = d_ch + ci;
+            // pipelined: chunk ci computes on aux stream b with buffer set b
+            // once the reduction of chunk ci-2 (same buffers) is done; the
+            // reductions stay on the caller's stream in chunk order, so F is
+            // accumulated exactly as in the serial schedule
+            const int b = (int)(ci & 1);
+            cudaStream_t cs = st;
+            if (pipe) {
+              cs = ax->cs[b];
+              a.G = b ? G2 : G;
+              a.part = b ? part2 : part;
+              if (ci >= 2) CU(cudaStreamWaitEvent(cs, ax->red[b], 0));
+            }
             if (mode == 1) {
-              CU(launch_far_colgen(a, l1, n_units, st));
+              CU(launch_far_colgen(a, l1, n_units, cs));
             } else if (mode == 2) {
-              CU(launch_far_pass1(a, l2, n_units, st));
-              CU(launch_far_rowdot(a, n_units, st));
+              CU(launch_far_pass1(a, l2, n_units, cs));
+              CU(launch_far_rowdot(a, n_units, cs));
             } else {
-              CU(launch_far_pass1(a, l2, n_units, st));
-              CU(launch_far_pass2(a, l1, n_units, st));
+              CU(launch_far_pass1(a, l2, n_units, cs));
+              CU(launch_far_pass2(a, l1, n_units, cs));
+            }
+            if (pipe) {
+              CU(cudaEventRecord(ax->done[b], cs));
+              CU(cudaStreamWaitEvent(st, ax->done[b], 0));
             }
             CU(launch_far_reduce(a, n_units, st));
+            if (pipe) CU(cudaEventRecord(ax->red[b], st));
           } else {
             int l1, l2;
             split_q(lq, &l1, &l2);
