@@ -160,21 +160,32 @@ def run_ours(args):
     lib = _lib.load()
     st = torch.cuda.current_stream()
 
-    def step(ev=None):
+    def step():
+        # one application, far + near field (the near field runs on its own
+        # stream beside the far-field chunks inside the library)
         F.zero_()
-        if ev:
+        grid.apply(reqs, C, F, _lib.FHTB_FAR | _lib.FHTB_NEAR)
+
+    def phases(n_rep):
+        """far-only / near-only applications, CUDA-event timed (diagnostic,
+        outside the timed region)"""
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        far, near = [], []
+        for _ in range(n_rep):
+            F.zero_()
             ev[0].record(st)
-        grid.apply(reqs, C, F, _lib.FHTB_FAR)
-        if ev:
+            grid.apply(reqs, C, F, _lib.FHTB_FAR)
             ev[1].record(st)
-        grid.apply(reqs, C, F, _lib.FHTB_NEAR)
-        if ev:
+            grid.apply(reqs, C, F, _lib.FHTB_NEAR)
             ev[2].record(st)
+            torch.cuda.synchronize()
+            far.append(ev[0].elapsed_time(ev[1]))
+            near.append(ev[1].elapsed_time(ev[2]))
+        return float(np.mean(far)), float(np.mean(near))
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clk = ClockSampler(local)
     if world > 1:
@@ -185,7 +196,7 @@ def run_ours(args):
     l0 = lib.fhtb_launch_count()
     t0.record(st)
     for k in range(args.steps):
-        step(evs[k])
+        step()
     t1.record(st)
     torch.cuda.synchronize()
     l1 = lib.fhtb_launch_count()
@@ -193,8 +204,6 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     ms = t0.elapsed_time(t1)
-    far_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
-    near_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -205,6 +214,7 @@ def run_ours(args):
     # parity spot check of the timed output against the direct-summation
     # sample rows and (rank 0) the CPU oracle
     out = F.cpu().numpy()
+    far_ms, near_ms = phases(max(2, min(args.steps, 5)))
 
     # end to end through the public API: pinned host in, host out
     if args.no_e2e:
@@ -260,7 +270,10 @@ def run_ours(args):
                    "gamma": GAMMA, "eps": EPS, "batch_per_gpu": batch, "M": params.m_terms,
                    "P": params.partitions, "blocks": len(scheme.blocks), "near_field_entries": scheme.mask_size(),
                    "l2": "inputs 512 MiB/GPU > 126 MB L2; no flush", "parallelism": "dp%d (vector sharding)" % world},
-        "phase_ms": {"far_field": far_ms, "near_field": near_ms},
+        "phase_ms": {"far_field": far_ms, "near_field": near_ms,
+                     "note": "far-only and near-only applications timed with CUDA events right after the "
+                             "timed region; the timed step runs both in one application, the near field "
+                             "on its own stream beside the far-field chunks"},
         "roofline": {"bound": "hbm", "kernel": "far field (pass 1 + pass 2 / column-generated pass 2 / row sums)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic_from_profile(), "model_bytes_per_vector": bpv,

@@ -34,6 +34,7 @@ int64_t g_near_chunk_cols = 8192;          // near-field column chunk per tile
 int g_far_prune = 1;                       // pruned side blocks (direct two-pass)
 int g_near_split = 1;                      // near field: order-parity classes
 int g_far_streams = 2;                     // far-field chunks in flight (direct two-pass)
+int g_near_overlap = 1;                    // near field on its own stream beside the far field
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -119,8 +120,8 @@ std::map<int, DevCtx> g_ctx;
 // chunks are computed on them two at a time and reduced in chunk order on the
 // caller's stream.
 struct AuxStreams {
-  cudaStream_t cs[2];
-  cudaEvent_t start, done[2], red[2];
+  cudaStream_t cs[3];                   // two far-field chunk streams, one near-field stream
+  cudaEvent_t start, done[2], red[2], nstart, ndone;
 };
 std::map<std::pair<int, cudaStream_t>, AuxStreams> g_aux;
 
@@ -133,11 +134,13 @@ int get_aux(cudaStream_t caller, AuxStreams** out) {
   if (it == g_aux.end()) {
     AuxStreams a;
     for (int i = 0; i < 2; ++i) {
-      CU(cudaStreamCreateWithFlags(&a.cs[i], cudaStreamNonBlocking));
       CU(cudaEventCreateWithFlags(&a.done[i], cudaEventDisableTiming));
       CU(cudaEventCreateWithFlags(&a.red[i], cudaEventDisableTiming));
     }
+    for (int i = 0; i < 3; ++i) CU(cudaStreamCreateWithFlags(&a.cs[i], cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&a.start, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&a.nstart, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&a.ndone, cudaEventDisableTiming));
     it = g_aux.emplace(key, a).first;
   }
   *out = &it->second;
@@ -480,6 +483,10 @@ int fhtb_set_option(const char* key, int64_t value) {
   if (!key) return fail(FHTB_EINVAL, "null key");
   if (!std::strcmp(key, "far_prune")) {
     g_far_prune = (int)value;
+    return FHTB_OK;
+  }
+  if (!std::strcmp(key, "near_overlap")) {
+    g_near_overlap = value ? 1 : 0;
     return FHTB_OK;
   }
   if (!std::strcmp(key, "far_streams")) {
@@ -869,6 +876,7 @@ size_t ws_need(const fhtb_grid* g, int n_req, int n_vec, int flags) {
     s += align_up(sizeof(ReqDesc) * ((size_t)std::max(n_req, 1) + 16 * (size_t)n_vec));
     s += align_up(sizeof(int2) * (n_vec + 2));
     s += align_up(sizeof(int) * (n_vec + 2)) + align_up(sizeof(int) * ((size_t)n_req + 2));
+    if (flags & FHTB_FAR) s += align_up(sizeof(double) * (size_t)n_vec * g->n_out);   // overlap buffer
   }
   return s + 4096;
 }
@@ -1096,6 +1104,96 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
   ReqDesc* d_req = cv.take<ReqDesc>(n_req);
   CU(cudaMemcpyAsync(d_req, rs.data(), n_req * sizeof(ReqDesc), cudaMemcpyHostToDevice, st));
 
+  // Near field concurrently with the far field (both requested): it runs on
+  // an auxiliary stream into a separate buffer Fn, added to F at the end on
+  // the caller's stream (F = far sum + near sum, as in the serial order).
+  const bool overlap = (flags & FHTB_NEAR) && (flags & FHTB_FAR) && !g->tiles.empty() &&
+                       !g->blocks.empty() && g_near_overlap;
+  cudaStream_t nst = st;
+  double* Fn = F;
+  int64_t ldfn = ldf;
+  AuxStreams* nax = nullptr;
+  if (overlap) {
+    if (int r = get_aux(st, &nax)) return r;
+    Fn = cv.take<double>((size_t)n_vec * g->n_out);
+    if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small");
+    ldfn = g->n_out;
+    nst = nax->cs[2];
+    CU(cudaEventRecord(nax->nstart, st));
+    CU(cudaStreamWaitEvent(nst, nax->nstart, 0));
+    CU(cudaMemsetAsync(Fn, 0, sizeof(double) * (size_t)n_vec * g->n_out, nst));
+  }
+  if ((flags & FHTB_NEAR) && !g->tiles.empty()) {
+    std::vector<int> q0, v0;
+    std::vector<int2> cls;
+    std::vector<ReqDesc> nreq;
+    int max_cols = 0;
+    bool identity = true;
+    for (int i = 0; i < (int)g->orders.size(); ++i) identity = identity && g->orders[i] == i;
+    const bool split = identity && g->orders.size() >= 3 && g_near_split;
+    if (split) {
+      if (int r = make_groups_split(rs, n_vec, (int)g->orders.size(), nreq, q0, v0, cls, &max_cols)) return r;
+    } else {
+      if (int r = make_groups(rs, n_vec, q0, v0, &max_cols)) return r;
+    }
+    std::vector<int> vstart, vcol;
+    vec_columns(split ? nreq : rs, q0, n_vec, vstart, vcol);
+    int* d_q0 = cv.take<int>(q0.size());
+    int* d_v0 = cv.take<int>(v0.size());
+    int* d_vs = cv.take<int>(vstart.size());
+    int* d_vc = cv.take<int>(vcol.size());
+    int2* d_cls = split ? cv.take<int2>(cls.size()) : nullptr;
+    ReqDesc* d_nreq = split ? cv.take<ReqDesc>(nreq.size()) : nullptr;
+    double* part = g->n_slots ? cv.take<double>((size_t)g->n_slots * n_vec * kNearRT) : nullptr;
+    if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small");
+    CU(cudaMemcpyAsync(d_q0, q0.data(), q0.size() * sizeof(int), cudaMemcpyHostToDevice, nst));
+    CU(cudaMemcpyAsync(d_v0, v0.data(), v0.size() * sizeof(int), cudaMemcpyHostToDevice, nst));
+    CU(cudaMemcpyAsync(d_vs, vstart.data(), vstart.size() * sizeof(int), cudaMemcpyHostToDevice, nst));
+    CU(cudaMemcpyAsync(d_vc, vcol.data(), vcol.size() * sizeof(int), cudaMemcpyHostToDevice, nst));
+    if (split) {
+      CU(cudaMemcpyAsync(d_cls, cls.data(), cls.size() * sizeof(int2), cudaMemcpyHostToDevice, nst));
+      CU(cudaMemcpyAsync(d_nreq, nreq.data(), nreq.size() * sizeof(ReqDesc), cudaMemcpyHostToDevice, nst));
+    }
+    NearArgs na;
+    std::memset(&na, 0, sizeof na);
+    na.tiles = g->d_tiles;
+    na.first = g->first;
+    na.stride = g->stride;
+    na.rowv = nullptr;
+    na.colv = nullptr;
+    na.gamma = g->gamma;
+    na.scale = M_PI / (double)g->L;
+    na.Ld = (double)g->L;
+    na.n_orders = (int)g->orders.size();
+    na.omax = 0;
+    na.orders_identity = 1;
+    for (int i = 0; i < na.n_orders; ++i) {
+      na.orders[i] = g->orders[i];
+      na.omax = std::max(na.omax, g->orders[i]);
+      if (g->orders[i] != i) na.orders_identity = 0;
+    }
+    na.jtab = ctx->jtab;
+    na.reqs = split ? d_nreq : d_req;
+    na.grp_q0 = d_q0;
+    na.grp_v0 = d_v0;
+    na.grp_cls = d_cls;
+    na.vstart = d_vs;
+    na.vcol = d_vc;
+    na.C = C;
+    na.ldc = ldc;
+    na.n_data_cols = g->n_data_cols;
+    na.F = Fn;
+    na.ldf = ldfn;
+    na.part = part;
+    na.part_stride = (long long)n_vec * kNearRT;
+    na.overwrite = 0;
+    na.shard = shard;
+    na.n_shards = n_shards;
+    CU(launch_near(na, (int)g->tiles.size(), (int)q0.size() - 1, max_cols, nst));
+    CU(launch_near_reduce(g->d_rts, (int)g->rts.size(), part, Fn, ldfn, n_vec, 0, nst));
+  }
+  if (overlap) CU(cudaEventRecord(nax->ndone, nst));
+
   // this shard's asymptotic term pairs [p0, p1) (all units) -- SURVEY 8(e)
   const int p0 = (int)((long long)g->M * shard / n_shards), p1 = (int)((long long)g->M * (shard + 1) / n_shards);
   int xl1 = 0, xrows = 0;
@@ -1223,74 +1321,9 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
     }
   }
 
-  if ((flags & FHTB_NEAR) && !g->tiles.empty()) {
-    std::vector<int> q0, v0;
-    std::vector<int2> cls;
-    std::vector<ReqDesc> nreq;
-    int max_cols = 0;
-    bool identity = true;
-    for (int i = 0; i < (int)g->orders.size(); ++i) identity = identity && g->orders[i] == i;
-    const bool split = identity && g->orders.size() >= 3 && g_near_split;
-    if (split) {
-      if (int r = make_groups_split(rs, n_vec, (int)g->orders.size(), nreq, q0, v0, cls, &max_cols)) return r;
-    } else {
-      if (int r = make_groups(rs, n_vec, q0, v0, &max_cols)) return r;
-    }
-    std::vector<int> vstart, vcol;
-    vec_columns(split ? nreq : rs, q0, n_vec, vstart, vcol);
-    int* d_q0 = cv.take<int>(q0.size());
-    int* d_v0 = cv.take<int>(v0.size());
-    int* d_vs = cv.take<int>(vstart.size());
-    int* d_vc = cv.take<int>(vcol.size());
-    int2* d_cls = split ? cv.take<int2>(cls.size()) : nullptr;
-    ReqDesc* d_nreq = split ? cv.take<ReqDesc>(nreq.size()) : nullptr;
-    double* part = g->n_slots ? cv.take<double>((size_t)g->n_slots * n_vec * kNearRT) : nullptr;
-    if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small");
-    CU(cudaMemcpyAsync(d_q0, q0.data(), q0.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(d_v0, v0.data(), v0.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(d_vs, vstart.data(), vstart.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(d_vc, vcol.data(), vcol.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    if (split) {
-      CU(cudaMemcpyAsync(d_cls, cls.data(), cls.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
-      CU(cudaMemcpyAsync(d_nreq, nreq.data(), nreq.size() * sizeof(ReqDesc), cudaMemcpyHostToDevice, st));
-    }
-    NearArgs na;
-    std::memset(&na, 0, sizeof na);
-    na.tiles = g->d_tiles;
-    na.first = g->first;
-    na.stride = g->stride;
-    na.rowv = nullptr;
-    na.colv = nullptr;
-    na.gamma = g->gamma;
-    na.scale = M_PI / (double)g->L;
-    na.Ld = (double)g->L;
-    na.n_orders = (int)g->orders.size();
-    na.omax = 0;
-    na.orders_identity = 1;
-    for (int i = 0; i < na.n_orders; ++i) {
-      na.orders[i] = g->orders[i];
-      na.omax = std::max(na.omax, g->orders[i]);
-      if (g->orders[i] != i) na.orders_identity = 0;
-    }
-    na.jtab = ctx->jtab;
-    na.reqs = split ? d_nreq : d_req;
-    na.grp_q0 = d_q0;
-    na.grp_v0 = d_v0;
-    na.grp_cls = d_cls;
-    na.vstart = d_vs;
-    na.vcol = d_vc;
-    na.C = C;
-    na.ldc = ldc;
-    na.n_data_cols = g->n_data_cols;
-    na.F = F;
-    na.ldf = ldf;
-    na.part = part;
-    na.part_stride = (long long)n_vec * kNearRT;
-    na.overwrite = 0;
-    na.shard = shard;
-    na.n_shards = n_shards;
-    CU(launch_near(na, (int)g->tiles.size(), (int)q0.size() - 1, max_cols, st));
-    CU(launch_near_reduce(g->d_rts, (int)g->rts.size(), part, F, ldf, n_vec, 0, st));
+  if (overlap) {
+    CU(cudaStreamWaitEvent(st, nax->ndone, 0));
+    CU(launch_add_rows(F, ldf, Fn, ldfn, n_vec, g->n_out, st));
   }
   return FHTB_OK;
 }

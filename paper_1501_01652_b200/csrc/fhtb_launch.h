@@ -89,6 +89,8 @@ extern int g_far_variant;         // tuning knob for the hot far-field sizes
 extern int g_chirp_variant;       // tuning knob for the chirp-z passes
 
 cudaError_t launch_near(const NearArgs& a, int n_tiles, int n_groups, int max_cols, cudaStream_t st);
+cudaError_t launch_add_rows(double* F, long long ldf, const double* Fn, long long ldn, int n_vec, long long n,
+                            cudaStream_t st);
 constexpr int kNearMaxCols = 128;   // request columns per near-field CTA (largest tile)
 cudaError_t launch_near_reduce(const NearRowTile* rt, int n_rt, const double* part, double* F,
                                long long ldf, int n_vec, int overwrite, cudaStream_t st);

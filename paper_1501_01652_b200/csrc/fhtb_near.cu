@@ -205,6 +205,26 @@ near_kernel(NearArgs a) {
   }
 }
 
+// F[v][j] += Fn[v][j]
+__global__ void add_rows_kernel(double* F, long long ldf, const double* Fn, long long ldn, int n_vec,
+                                long long n) {
+  const long long tot = (long long)n_vec * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const long long v = e / n, j = e % n;
+    F[v * ldf + j] += Fn[v * ldn + j];
+  }
+}
+
+cudaError_t launch_add_rows(double* F, long long ldf, const double* Fn, long long ldn, int n_vec, long long n,
+                            cudaStream_t st) {
+  const long long tot = (long long)n_vec * n;
+  long long b = (tot + 255) / 256;
+  if (b > 148 * 32) b = 148 * 32;
+  if (b < 1) return cudaSuccess;
+  note_launch(), add_rows_kernel<<<(unsigned)b, 256, 0, st>>>(F, ldf, Fn, ldn, n_vec, n);
+  return cudaGetLastError();
+}
+
 // Sum column-chunk partials of one row tile in chunk order.
 __global__ void near_reduce_kernel(const NearRowTile* rt, const double* part, double* F,
                                    long long ldf, int n_vec, int overwrite) {
