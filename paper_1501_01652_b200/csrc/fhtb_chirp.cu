@@ -25,7 +25,7 @@
 
 namespace fhtb {
 
-int g_chirp_variant = 0;   // tuning bits (performance only): 1 = pass 3 unbounded regs, 2 = pass 1 unbounded
+int g_chirp_variant = 0;   // tuning bits (performance only): 1 = pass 3 unbounded regs
 
 __device__ __forceinline__ double ipow_c(double x, int p) {
   double r = 1.0;
@@ -50,12 +50,19 @@ __device__ __forceinline__ double2 qtw_s(const FarArgs& a, long long m, int sign
 }
 
 // ------------------------------------------------------------------ pass 1
-template <int N2, int E, int W, int MINB>
+// HZ: the block's columns m < Mn <= Q/2 lie in the lower half of every
+// column (n2 < N2/2), so the upper half of each thread's slots is zero and
+// the first radix pass is the half-zero DFT.  The four-step twiddles
+// e^{-2 pi i n1 k2/Q} of the thread's outputs are the same for every term:
+// built once into shared memory (thread-private slot-major slots).
+template <int N2, int E, int W, int MINB, bool HZ>
 __global__ void __launch_bounds__(W * (N2 / E), MINB)
 chirp_pass1_kernel(FarArgs a) {
   constexpr int T = N2 / E;
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
   constexpr int NP = N2 + PAD;
+  constexpr int EH = HZ ? E / 2 : E;
+  constexpr int NTH = W * T;
   extern __shared__ double2 sm2[];
   const int tid = threadIdx.x, w = tid % W, tt = tid / W;
   const int Q1 = a.L1;
@@ -68,9 +75,9 @@ chirp_pass1_kernel(FarArgs a) {
   const long long cA = max(max(B.c0, R.col_lo), 1LL);
   const long long cB = min(B.c1, min(a.n_data_cols + 1, a.L + 1));
   const long long k0 = a.first, s = a.stride, n0 = B.c0, L = a.L;
-  double br[E], bi[E], iw[E];
+  double br[EH], bi[EH], iw[EH];
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
+  for (int e = 0; e < EH; ++e) {
     const long long m = n1 + (long long)Q1 * (tt + T * e);
     const long long n = n0 + m;
     br[e] = bi[e] = iw[e] = 0.0;
@@ -87,12 +94,15 @@ chirp_pass1_kernel(FarArgs a) {
     }
   }
   double2* sm = sm2 + w * NP;
+  double2* qt = sm2 + W * NP + tid;
+#pragma unroll
+  for (int q = 0; q < E; ++q) qt[q * NTH] = qtw_s(a, n1 * fft_out_index<N2, E>(tt, q), -1);
   const double2* tw = a.tw + (N2 - 2);
   const int nterm = 2 * a.M;
   const int t0 = 2 * a.p0, t1 = 2 * a.p1;     // this shard's terms
   for (int i = 0; i < t0; ++i) {
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
+    for (int e = 0; e < EH; ++e) {
       br[e] *= iw[e];
       bi[e] *= iw[e];
     }
@@ -100,18 +110,20 @@ chirp_pass1_kernel(FarArgs a) {
   for (int i = t0; i < t1; ++i) {
     double2 z[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
+    for (int e = 0; e < EH; ++e) {
       z[e] = make_double2(br[e], bi[e]);
       br[e] *= iw[e];
       bi[e] *= iw[e];
     }
+#pragma unroll
+    for (int e = EH; e < E; ++e) z[e] = make_double2(0.0, 0.0);
     __syncthreads();
-    block_fft<N2, E, -1>(z, sm, tt, tw);
+    block_fft<N2, E, -1, HZ>(z, sm, tt, tw);
     double2* G = a.G + (long long)(ul * nterm + i) * Q;
 #pragma unroll
     for (int q = 0; q < E; ++q) {
       const int k2 = fft_out_index<N2, E>(tt, q);
-      G[(long long)k2 * Q1 + n1] = cmul(z[q], qtw_s(a, n1 * k2, -1));
+      G[(long long)k2 * Q1 + n1] = cmul(z[q], qt[q * NTH]);
     }
   }
 }
@@ -391,12 +403,12 @@ static int pick_w(int N2) {
 }
 
 template <int N2, int W>
-static cudaError_t c1_w(const FarArgs& a, int n_units, cudaStream_t st) {
+static cudaError_t c1_w(const FarArgs& a, int n_units, int hz, cudaStream_t st) {
   constexpr int E = N2 >= 8 ? 8 : N2;
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
-  const int smem = W * (N2 + PAD) * 16;
+  const int smem = (W * (N2 + PAD) + W * N2) * 16;   // FFT buffers + four-step twiddles
   constexpr int MB = (W * (N2 / E)) >= 256 ? 2 : 1;
-  auto k = (g_chirp_variant & 2) ? chirp_pass1_kernel<N2, E, W, 1> : chirp_pass1_kernel<N2, E, W, MB>;
+  auto k = (hz && E >= 8) ? chirp_pass1_kernel<N2, E, W, MB, true> : chirp_pass1_kernel<N2, E, W, MB, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   note_launch(), k<<<dim3(a.L1 / W, n_units), W * (N2 / E), smem, st>>>(a);
@@ -449,8 +461,8 @@ static cudaError_t pp1_w(const double2* in, double2* out, const FarArgs& a, cuda
     case 12: MACRO(4096); case 13: MACRO(8192);                                  \
   }
 
-cudaError_t launch_chirp_pass1(const FarArgs& a, int logN2, int n_units, cudaStream_t st) {
-#define M1(N) FHTB_W_DISPATCH(c1_w, N, a, n_units, st)
+cudaError_t launch_chirp_pass1(const FarArgs& a, int logN2, int n_units, int hz, cudaStream_t st) {
+#define M1(N) FHTB_W_DISPATCH(c1_w, N, a, n_units, hz, st)
   FHTB_SIZE_SWITCH(logN2, M1)
 #undef M1
   return cudaErrorInvalidValue;

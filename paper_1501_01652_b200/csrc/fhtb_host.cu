@@ -833,19 +833,27 @@ void plan_far(const fhtb_grid* g, const std::vector<ReqDesc>& rs, FarPlan& fp, i
     return;
   }
   // chirp mode: group by filter length, keep vector order inside a group
+  // key: 2 log2 Q + hz, hz = the block's columns fill at most half of Q (the
+  // pass-1 FFT input is then zero in its upper half)
+  auto ckey = [&](const UnitDesc& u) {
+    const BlockDesc& b = g->bdesc[u.block];
+    return 2 * b.logQ + ((2 * b.Mn <= (1LL << b.logQ)) ? 1 : 0);
+  };
   std::vector<int> logs;
-  for (auto& u : all) logs.push_back(g->bdesc[u.block].logQ);
+  for (auto& u : all) logs.push_back(ckey(u));
   std::sort(logs.begin(), logs.end());
   logs.erase(std::unique(logs.begin(), logs.end()), logs.end());
-  for (int lq : logs) {
+  for (int key : logs) {
+    const int lq = key / 2;
     const long long start = (long long)fp.units.size();
     for (auto& u : all)
-      if (g->bdesc[u.block].logQ == lq) fp.units.push_back(u);
+      if (ckey(u) == key) fp.units.push_back(u);
     const long long n = (long long)fp.units.size() - start;
     const size_t ub = unit_bytes_q(g, lq);
     const long long cu = chunk_for(ub, n);
     for (long long u0 = 0; u0 < n; u0 += cu) {
       fp.chunks.push_back(make_int2((int)(start + u0), (int)(start + std::min(n, u0 + cu))));
+      fp.chunk_key.push_back(key % 2);
       fp.chunk_logq.push_back(lq);
     }
     fp.g_bytes = std::max(fp.g_bytes, ub * (size_t)cu);
@@ -1311,7 +1319,7 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
             a.L1 = 1 << l1;
             a.L2 = 1 << l2;
             CU(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)n_units * g->n_out, st));
-            CU(launch_chirp_pass1(a, l2, n_units, st));
+            CU(launch_chirp_pass1(a, l2, n_units, fp.chunk_key[ci], st));
             CU(launch_chirp_pass2(a, l1, n_units, st));
             CU(launch_chirp_pass3(a, l2, n_units, st));
             CU(launch_chirp_reduce(a, n_units, st));

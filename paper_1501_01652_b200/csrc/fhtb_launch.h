@@ -108,7 +108,8 @@ cudaError_t launch_far_rowdot(const FarArgs& a, int n_units, cudaStream_t st);
 cudaError_t launch_cs_table(double2* cs, long long L, double gamma, double pi_over_L, cudaStream_t st);
 
 // chirp mode (any grid length, strided output rows)
-cudaError_t launch_chirp_pass1(const FarArgs& a, int logN2, int n_units, cudaStream_t st);
+// hz: every unit's columns fit in the lower half of Q (half-zero first pass)
+cudaError_t launch_chirp_pass1(const FarArgs& a, int logN2, int n_units, int hz, cudaStream_t st);
 cudaError_t launch_chirp_pass2(const FarArgs& a, int logN1, int n_units, cudaStream_t st);
 cudaError_t launch_chirp_pass3(const FarArgs& a, int logN2, int n_units, cudaStream_t st);
 cudaError_t launch_chirp_reduce(const FarArgs& a, int n_units, cudaStream_t st);
