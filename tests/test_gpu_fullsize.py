@@ -1,0 +1,97 @@
+"""BASELINE.json full-size configurations, checked through size-independent
+properties (the CPU oracle needs ~27 s per cfg2 vector, so it is used in the
+bench, not here):
+
+* direct fp64 summation on sampled rows: every row of the fast transform
+  within 10 eps ||c||_1 of sum_n c_n J_nu(r_k omega_n) evaluated by the GPU
+  direct kernel (fhtb_direct_apply), rows sampled across all partition blocks
+  plus the first and last rows;
+* linearity: f(a c1 + b c2) = a f(c1) + b f(c2) within the same bound;
+* run-to-run determinism (bitwise) and batch independence (a vector gives
+  the same bits alone as inside a batch).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1501_01652_b200 as fh
+from paper_1501_01652_b200.fourier_bessel import _direct_apply
+
+pytestmark = pytest.mark.gpu
+
+
+def _sample_rows(n, count, seed):
+    rng = np.random.default_rng(seed)
+    rows = set(rng.integers(1, n + 1, count).tolist())
+    rows |= {1, 2, 3, n - 1, n} | {int(n * f) for f in (0.001, 0.01, 0.1, 0.5)}
+    return np.array(sorted(r for r in rows if 1 <= r <= n), dtype=np.int64)
+
+
+def _direct_rows(row_val, col_val, nu, C):
+    """out[v][i] = sum_n C[v][n-1] J_nu(row_val[i] * col_val[n-1]) (GPU direct sums)."""
+    out = torch.zeros((C.shape[0], row_val.numel()), dtype=torch.float64, device=C.device)
+    reqs = [dict(vec=v, terms=[(nu, 1.0)]) for v in range(C.shape[0])]
+    _direct_apply(row_val, col_val, C.shape[1], [nu], reqs, C, out)
+    return out
+
+
+def _cfg2_inputs(n, batch, seed):
+    rows = [np.random.default_rng([seed, n, b]).standard_normal(n) / np.arange(1, n + 1) for b in range(batch)]
+    return torch.from_numpy(np.stack(rows)).cuda()
+
+
+@pytest.mark.parametrize("eps", [1e-3, 1e-8, 1e-15])
+def test_cfg2_fullsize_vs_direct_rows(cuda_dev, eps):
+    n, nu, gamma = 2 ** 20, 4, 4.0
+    C = _cfg2_inputs(n, 4, 7)
+    params = fh.select_params(nu, n, eps, gamma=gamma)
+    F = fh.schlomilch_fast(params, C)
+    rows = _sample_rows(n, 200, 11)
+    k = torch.from_numpy(rows).to(cuda_dev)
+    row_val = (k.double() / n).contiguous()
+    col_val = ((torch.arange(1, n + 1, dtype=torch.float64, device=cuda_dev) + gamma) * np.pi).contiguous()
+    ref = _direct_rows(row_val, col_val, nu, C)
+    got = F[:, k - 1]
+    tol = 10 * eps * C.abs().sum(1)
+    err = (got - ref).abs().max(1).values
+    assert bool((err <= tol).all()), (err.cpu().numpy(), tol.cpu().numpy())
+
+
+def test_cfg2_fullsize_linearity_determinism_batch_independence(cuda_dev):
+    n, nu, gamma, eps = 2 ** 20, 4, 4.0, 1e-15
+    C = _cfg2_inputs(n, 2, 3)
+    params = fh.select_params(nu, n, eps, gamma=gamma)
+    F = fh.schlomilch_fast(params, C)
+    a, b = 0.75, -1.5
+    mix = fh.schlomilch_fast(params, (a * C[0] + b * C[1]).contiguous())
+    tol = 10 * eps * (abs(a) * float(C[0].abs().sum()) + abs(b) * float(C[1].abs().sum()))
+    assert float((mix - (a * F[0] + b * F[1])).abs().max()) <= tol
+    assert torch.equal(fh.schlomilch_fast(params, C), F)                   # run to run
+    assert torch.equal(fh.schlomilch_fast(params, C[1].contiguous()), F[1])  # batch independence
+
+
+def test_fb_cfg3_fullsize_vs_direct_rows(cuda_dev):
+    n, eps = 2 ** 18, 1e-12
+    roots = fh.bessel_roots_j0(n)
+    C = torch.from_numpy(np.stack([np.random.default_rng([1, n, b]).uniform(-1, 1, n) for b in range(2)])).cuda()
+    F = fh.fourier_bessel_eval(0, C, eps, roots=roots)
+    rows = _sample_rows(n, 150, 5)
+    k = torch.from_numpy(rows).to(cuda_dev)
+    r_dev, _ = roots.device_arrays()
+    ref = _direct_rows((k.double() / n).contiguous(), r_dev[:n].contiguous(), 0, C)
+    err = (F[:, k - 1] - ref).abs().max(1).values
+    tol = 10 * eps * C.abs().sum(1)
+    assert bool((err <= tol).all()), (err.cpu().numpy(), tol.cpu().numpy())
+
+
+def test_dht_cfg4_fullsize_vs_direct(cuda_dev):
+    n, eps = 2 ** 16, 1e-15
+    plan = fh.dht_plan(n, eps)
+    C = torch.from_numpy(np.stack([np.random.default_rng([1, n, b]).standard_normal(n) for b in range(2)])).cuda()
+    F = fh.dht(plan, C)
+    ref = fh.dht_direct(plan, C)                      # O(N^2) = 4.3e9 J0 per vector on the GPU
+    err = (F - ref).abs().max(1).values
+    tol = 10 * eps * C.abs().sum(1)
+    assert bool((err <= tol).all()), (err.cpu().numpy(), tol.cpu().numpy())
+    assert torch.equal(fh.dht(plan, C), F)
