@@ -98,7 +98,8 @@ def load(path=LIB_PATH):
             for env, key in (("FHTB_FAR_VARIANT", b"far_variant"), ("FHTB_CHIRP_VARIANT", b"chirp_variant"),
                              ("FHTB_FAR_CHUNK_BYTES", b"far_chunk_bytes"),
                              ("FHTB_NEAR_CHUNK_COLS", b"near_chunk_cols"), ("FHTB_NEAR_SPLIT", b"near_split"), ("FHTB_FAR_STREAMS", b"far_streams"),
-                             ("FHTB_NEAR_OVERLAP", b"near_overlap")):
+                             ("FHTB_NEAR_OVERLAP", b"near_overlap"),
+                             ("FHTB_FAR_PRUNE_ROWS", b"far_prune_rows")):
                 if os.environ.get(env):
                     lib.fhtb_set_option(key, int(os.environ[env]))
             _lib = lib

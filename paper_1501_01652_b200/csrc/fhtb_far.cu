@@ -76,7 +76,9 @@ __device__ __forceinline__ void unit_cols(const FarArgs& a, const ReqDesc& R, co
 // memory as rows [k2][w] (reusing the FFT buffer) and written to G by 2D
 // tensor stores (boxes of 2W doubles x BR rows), so the strided W*16-byte row
 // segments do not go through the LSU path one warp instruction at a time.
-template <int N2, int E, int W, int MINB, bool TMA>
+// QT: four-step twiddles staged in shared memory (else computed per use,
+// for the large columns whose table would not fit beside the FFT buffer).
+template <int N2, int E, int W, int MINB, bool TMA, bool QT = true>
 __global__ void __launch_bounds__(W * (N2 / E), MINB)
 far_pass1_kernel(FarArgs a, const __grid_constant__ CUtensorMap gmap) {
   constexpr int T = N2 / E;
@@ -110,7 +112,8 @@ far_pass1_kernel(FarArgs a, const __grid_constant__ CUtensorMap gmap) {
   double2* qt = sm2 + W * NP + tid;
   constexpr int NTH = W * T;
 #pragma unroll
-  for (int s = 0; s < E; ++s) qt[s * NTH] = qtw(a, n1 * fft_out_index<N2, E>(tt, s));
+  for (int s = 0; s < E; ++s)
+    if (QT) qt[s * NTH] = qtw(a, n1 * fft_out_index<N2, E>(tt, s));
   for (int p = 0; p < a.p0; ++p) {          // advance to the shard's first pair
 #pragma unroll
     for (int e = 0; e < EH; ++e) v[e] = (v[e] * iw[e]) * iw[e];
@@ -136,7 +139,7 @@ far_pass1_kernel(FarArgs a, const __grid_constant__ CUtensorMap gmap) {
 #pragma unroll
       for (int s = 0; s < E; ++s) {
         const int k2 = fft_out_index<N2, E>(tt, s);
-        sm2[k2 * W + w] = cmul(z[s], qt[s * NTH]);
+        sm2[k2 * W + w] = cmul(z[s], QT ? qt[s * NTH] : qtw(a, n1 * k2));
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
@@ -158,14 +161,15 @@ far_pass1_kernel(FarArgs a, const __grid_constant__ CUtensorMap gmap) {
       for (int s = 0; s < E; ++s) {
         const int k2 = fft_out_index<N2, E>(tt, s);
         const int2 oj = __ldg(a.xrow + k2);
-        a.G[oj.x * a.xchunk + (((long long)(ul * a.M + p) * a.xrows + oj.y) << a.xlog) + nl] = cmul(z[s], qt[s * NTH]);
+        a.G[oj.x * a.xchunk + (((long long)(ul * a.M + p) * a.xrows + oj.y) << a.xlog) + nl] =
+            cmul(z[s], QT ? qt[s * NTH] : qtw(a, n1 * k2));
       }
     } else {
       double2* G = a.G + ((long long)(ul * a.M + p) * N2) * L1;
 #pragma unroll
       for (int s = 0; s < E; ++s) {
         const int k2 = fft_out_index<N2, E>(tt, s);
-        G[(long long)k2 * L1 + n1] = cmul(z[s], qt[s * NTH]);
+        G[(long long)k2 * L1 + n1] = cmul(z[s], QT ? qt[s * NTH] : qtw(a, n1 * k2));
       }
     }
   }
@@ -725,15 +729,15 @@ static bool g_tmap(CUtensorMap* m, const FarArgs& a, int n_units, int W, int BR)
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int N2, int E, int W, int MINB>
+template <int N2, int E, int W, int MINB, bool QT = true>
 static cudaError_t p1_t(const FarArgs& a, int n_units, cudaStream_t st) {
   constexpr int T = N2 / E;
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
-  const int smem = (W * (N2 + PAD) + W * N2) * 16;   // FFT buffers (staging) + four-step twiddles
+  const int smem = (W * (N2 + PAD) + (QT ? W * N2 : 0)) * 16;   // FFT buffers (staging) + four-step twiddles
   CUtensorMap m;
   std::memset(&m, 0, sizeof m);
   const bool tma = !a.xw && !(g_far_variant & 0x10000) && g_tmap(&m, a, n_units, W, N2 < 256 ? N2 : 256);
-  auto k = tma ? far_pass1_kernel<N2, E, W, MINB, true> : far_pass1_kernel<N2, E, W, MINB, false>;
+  auto k = tma ? far_pass1_kernel<N2, E, W, MINB, true, QT> : far_pass1_kernel<N2, E, W, MINB, false, QT>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int cols = a.xw ? a.L1 / a.xw : a.L1;      // exchange mode: this rank's column slab
@@ -747,6 +751,8 @@ static cudaError_t p1_d(const FarArgs& a, int n_units, cudaStream_t st) {
   constexpr int E = N2 >= 16 ? 16 : N2;
   // 512-point columns: 128-thread CTAs, 3 per SM (as the tuned 1024 shape)
   if (N2 == 512) return p1_t<N2, E, 4, 3>(a, n_units, st);
+  // 4096-point columns (narrow-row blocks): twiddles computed per use, 2 CTAs/SM
+  if (N2 == 4096) return p1_t<N2, E, 1, 2, false>(a, n_units, st);
   constexpr int W = N2 >= 4096 ? 1 : 4096 / N2;
   return p1_t<N2, E, W, 1>(a, n_units, st);
 }

@@ -35,6 +35,7 @@ int g_far_prune = 1;                       // pruned side blocks (direct two-pas
 int g_near_split = 1;                      // near field: order-parity classes
 int g_far_streams = 2;                     // far-field chunks in flight (direct two-pass)
 int g_near_overlap = 1;                    // near field on its own stream beside the far field
+int g_prune_rows = 11;                     // narrow-row blocks: rows below 2^g_prune_rows
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -485,6 +486,11 @@ int fhtb_set_option(const char* key, int64_t value) {
     g_far_prune = (int)value;
     return FHTB_OK;
   }
+  if (!std::strcmp(key, "far_prune_rows")) {
+    if (value < 10 || value > 12) return fail(FHTB_EINVAL, "far_prune_rows must be 10..12");
+    g_prune_rows = (int)value;
+    return FHTB_OK;
+  }
   if (!std::strcmp(key, "near_overlap")) {
     g_near_overlap = value ? 1 : 0;
     return FHTB_OK;
@@ -675,7 +681,7 @@ int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
       if (g_far_prune && lc <= 12 && lc < g->logQ) {
         x.dmode = 1;                 // narrow columns: pass 1 degenerates
         x.dlogL1 = lc;
-      } else if (g_far_prune && lr <= 11 && lr < g->logQ && g->logQ - lr <= 13) {
+      } else if (g_far_prune && lr <= g_prune_rows && lr < g->logQ && g->logQ - lr <= 13) {
         x.dmode = 2;                 // narrow rows: pass 2 collapses to two sums
         x.dlogL1 = g->logQ - lr;
       }
