@@ -273,7 +273,10 @@ far_pass2_kernel(FarArgs a) {
   const double2* tw = a.tw + (N1 - 2);
   const int xj = XCH ? __ldg(a.xrow + myk2).y : 0;
 
-  int kq[NQ];
+  // E <= 8: the shared-memory offsets of Z[k] and Z[2L-k] are kept per slot
+  // (registers allow it); E = 16 recomputes them per pair
+  constexpr bool PRE = (E <= 8 && N1 >= 1024);
+  int kq[NQ], oz[PRE ? NQ : 1], op[PRE ? NQ : 1];
   double ir[NQ], rp[HOR ? 1 : NQ];
   double2 acc[NQ];
 #pragma unroll
@@ -290,6 +293,11 @@ far_pass2_kernel(FarArgs a) {
     kq[q] = k;
     acc[q] = make_double2(0.0, 0.0);
     ir[q] = k ? a.Ld / (double)k : 0.0;
+    if (PRE) {
+      const int kp = 2 * L - k;
+      oz[PRE ? q : 0] = k ? (((k & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(k / L2) : 0;
+      op[PRE ? q : 0] = k ? (((kp & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(kp / L2) : 0;
+    }
     if (!HOR) {
       double post = 1.0;
       if (k && R.pr) post = ipow_f((double)k / a.Ld, R.pr);
@@ -364,8 +372,8 @@ far_pass2_kernel(FarArgs a) {
       const int k = kq[q];
       if (!k) continue;
       const int kp = 2 * L - k;
-      const double2 Zk = sm2[(((k & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(k / L2)];
-      const double2 Zp = cconj(sm2[(((kp & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(kp / L2)]);
+      const double2 Zk = sm2[PRE ? oz[PRE ? q : 0] : (((k & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(k / L2)];
+      const double2 Zp = cconj(sm2[PRE ? op[PRE ? q : 0] : (((kp & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(kp / L2)]);
       // 2 Ya, 2 Yb (the factor 1/2 is folded into r_0)
       double2 Ya = make_double2(Zk.x + Zp.x, Zk.y + Zp.y);
       double2 Yb = make_double2(Zk.y - Zp.y, Zp.x - Zk.x);
