@@ -156,6 +156,25 @@ int fhtb_apply_x(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, co
                  void* recv, size_t xbytes, fhtb_exchange_fn exchange, void* user, void* ws, size_t ws_bytes,
                  void* stream);
 
+/* fhtb_apply(FAR|NEAR) from HOST memory to HOST memory: the end-to-end
+ * form of schlomilch.py:389-396 / :436-468 for a caller holding host arrays
+ * (the reference's own calling convention, numpy in and out).  C_host
+ * (n_vec rows of n_data_cols, leading dimension ldc_host) is copied in
+ * n_groups vector groups on a copy stream; the far field of group g starts
+ * as soon as its rows have landed, the near field of the whole batch runs on
+ * its own stream once all rows are in, and the finished rows of group g are
+ * copied out to F_host (n_vec rows of n_out, overwritten) while later groups
+ * compute.  Pinned host memory gives the overlap; pageable memory is
+ * accepted (copies then serialise).  The result equals fhtb_apply on device
+ * copies of C, F = 0, bit for bit (reductions are independent of the
+ * grouping).  Device buffers are carved from ws
+ * (fhtb_apply_host_workspace).  Asynchronous on `stream`: F_host is valid
+ * after the stream synchronises. */
+size_t fhtb_apply_host_workspace(const fhtb_grid* g, int32_t n_req, int32_t n_vec, int32_t flags);
+int fhtb_apply_host(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C_host,
+                    int64_t ldc_host, int32_t n_vec, double* F_host, int64_t ldf_host, int32_t flags,
+                    int32_t n_groups, void* ws, size_t ws_bytes, void* stream);
+
 /* Direct sums with rank-1 arguments z = row_val[k] * col_val[n] over a full
  * n_rows x n_cols rectangle: fourier_bessel.py:148-172 (low columns),
  * dht.py:82-94 (direct rows), and the O(N^2) oracles schlomilch.py:223-229,

@@ -70,6 +70,9 @@ EXPORTS = {
     "fhtb_apply_x_workspace": (ctypes.c_size_t, [vp, i32, i32, i32, i32, ctypes.c_size_t]),
     "fhtb_apply_x": (i32, [vp, ctypes.POINTER(Request), i32, vp, i64, i32, vp, i64, i32, i32, i32, vp, vp,
                            ctypes.c_size_t, EXCHANGE_FN, vp, vp, ctypes.c_size_t, vp]),
+    "fhtb_apply_host_workspace": (ctypes.c_size_t, [vp, i32, i32, i32]),
+    "fhtb_apply_host": (i32, [vp, ctypes.POINTER(Request), i32, vp, i64, i32, vp, i64, i32, i32, vp,
+                              ctypes.c_size_t, vp]),
     "fhtb_direct_workspace": (ctypes.c_size_t, [ctypes.POINTER(DirectDesc), i32, i32]),
     "fhtb_direct_apply": (i32, [ctypes.POINTER(DirectDesc), ctypes.POINTER(Request), i32, vp,
                                 i64, i32, vp, i64, i32, vp, ctypes.c_size_t, vp]),

@@ -281,12 +281,14 @@ __global__ void chirp_reduce_kernel(FarArgs a, int n_units) {
   int u = 0;
   while (u < n_units) {
     const int vec = a.units[a.u0 + u].vec;
-    double s = 0.0;
+    // unit by unit into F: independent of chunk boundaries (far_reduce_kernel)
+    double* f = a.F + (long long)vec * a.ldf + j;
+    double s = *f;
     while (u < n_units && a.units[a.u0 + u].vec == vec) {
       s += a.part[(long long)u * a.part_stride + j];
       ++u;
     }
-    a.F[(long long)vec * a.ldf + j] += s;
+    *f = s;
   }
 }
 

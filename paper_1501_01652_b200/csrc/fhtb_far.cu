@@ -676,8 +676,11 @@ far_pass2x_kernel(FarArgs a) {
   }
 }
 
-// F[vec][j] += sum over the chunk's units of vec whose block holds row j,
-// in unit order.  Units of one vector are contiguous in the chunk.
+// F[vec][j] += each partial of the chunk's units of vec whose block holds row
+// j, one at a time in unit order.  Units of one vector are contiguous in the
+// chunk.  Adding unit by unit (not the chunk's sum) makes F independent of
+// where the chunk boundaries fall, so a vector's result does not depend on
+// the rest of the batch (fhtb_apply_host runs vector groups separately).
 __global__ void far_reduce_kernel(FarArgs a, int n_units) {
   const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (j >= a.n_out) return;
@@ -685,7 +688,8 @@ __global__ void far_reduce_kernel(FarArgs a, int n_units) {
   int u = 0;
   while (u < n_units) {
     const int vec = a.units[a.u0 + u].vec;
-    double s = 0.0;
+    double* f = a.F + (long long)vec * a.ldf + j;
+    double s = *f;
     bool any = false;
     while (u < n_units && a.units[a.u0 + u].vec == vec) {
       const BlockDesc& B = a.blocks[a.units[a.u0 + u].block];
@@ -695,7 +699,7 @@ __global__ void far_reduce_kernel(FarArgs a, int n_units) {
       }
       ++u;
     }
-    if (any) a.F[(long long)vec * a.ldf + j] += s;
+    if (any) *f = s;
   }
 }
 

@@ -998,6 +998,170 @@ int fhtb_apply_x(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, co
 
 }  // extern "C"
 
+// ------------------------------------------------ host-buffer application
+// fhtb_apply_host: the whole batch from host memory to host memory, with the
+// copies overlapped with the far field.  Vector groups g = 0..G-1:
+//   h2d stream : C_dev[g] <- C_host[g]                       (event in[g])
+//   near stream: after in[G-1], the near field of ALL vectors into Fn
+//                (one batched call: the Bessel tiles are shared by the batch)
+//   caller     : after in[g], F_dev[g] = 0; far field of group g; after the
+//                near field, F_dev[g] += Fn[g]                 (event fin[g])
+//   d2h stream : after fin[g], F_host[g] <- F_dev[g]
+// Per vector this is the arithmetic of fhtb_apply(FAR|NEAR): far partials
+// added unit by unit in plan order (independent of the grouping), then the
+// near sum.  So the result equals fhtb_apply on device copies bit for bit.
+namespace {
+constexpr int kMaxHostGroups = 64;
+struct HostAux {
+  cudaStream_t h2d, d2h, near;
+  cudaEvent_t in[kMaxHostGroups], fin[kMaxHostGroups], nstart, ndone;
+};
+std::map<std::pair<int, cudaStream_t>, HostAux> g_haux;
+
+int get_haux(cudaStream_t caller, HostAux** out) {
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_pair(dev, caller);
+  auto it = g_haux.find(key);
+  if (it == g_haux.end()) {
+    HostAux h;
+    CU(cudaStreamCreateWithFlags(&h.h2d, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&h.d2h, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&h.near, cudaStreamNonBlocking));
+    for (int i = 0; i < kMaxHostGroups; ++i) {
+      CU(cudaEventCreateWithFlags(&h.in[i], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&h.fin[i], cudaEventDisableTiming));
+    }
+    CU(cudaEventCreateWithFlags(&h.nstart, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h.ndone, cudaEventDisableTiming));
+    it = g_haux.emplace(key, h).first;
+  }
+  *out = &it->second;
+  return FHTB_OK;
+}
+
+struct HostLayout {
+  size_t c_off, f_off, fn_off, far_off, far_bytes, near_off, near_bytes, total;
+};
+
+HostLayout host_layout(const fhtb_grid* g, int32_t n_req, int32_t n_vec, int32_t flags) {
+  HostLayout h;
+  size_t s = 0;
+  h.c_off = s;
+  s += align_up(sizeof(double) * (size_t)n_vec * g->n_data_cols);
+  h.f_off = s;
+  s += align_up(sizeof(double) * (size_t)n_vec * g->n_out);
+  const bool near = (flags & FHTB_NEAR) && !g->tiles.empty();
+  h.fn_off = s;
+  if (near && (flags & FHTB_FAR)) s += align_up(sizeof(double) * (size_t)n_vec * g->n_out);
+  h.far_off = s;
+  h.far_bytes = (flags & FHTB_FAR) ? ws_need(g, n_req, n_vec, FHTB_FAR) : 0;
+  s += align_up(h.far_bytes);
+  h.near_off = s;
+  h.near_bytes = near ? ws_need(g, n_req, n_vec, FHTB_NEAR) : 0;
+  s += align_up(h.near_bytes);
+  h.total = s + 4096;
+  return h;
+}
+}  // namespace
+
+extern "C" {
+
+size_t fhtb_apply_host_workspace(const fhtb_grid* g, int32_t n_req, int32_t n_vec, int32_t flags) {
+  if (!g) return 0;
+  return host_layout(g, n_req, n_vec, flags).total;
+}
+
+int fhtb_apply_host(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C_host,
+                    int64_t ldc_host, int32_t n_vec, double* F_host, int64_t ldf_host, int32_t flags,
+                    int32_t n_groups, void* ws, size_t ws_bytes, void* stream) {
+  if (!g) return fail(FHTB_EINVAL, "null grid");
+  if (n_req < 0 || n_vec < 0) return fail(FHTB_EINVAL, "negative counts");
+  if (!C_host || !F_host) return fail(FHTB_EINVAL, "null host buffer");
+  if (ldc_host < g->n_data_cols || ldf_host < g->n_out) return fail(FHTB_EINVAL, "host leading dimension too small");
+  if (n_vec == 0) return FHTB_OK;
+  for (int q = 0; q < n_req; ++q)
+    if (reqs[q].vec < 0 || reqs[q].vec >= n_vec) return fail(FHTB_EINVAL, "request vec out of range");
+  const HostLayout hl = host_layout(g, n_req, n_vec, flags);
+  if (ws_bytes < hl.total) return fail(FHTB_EINVAL, "workspace too small");
+  char* base = (char*)align_up((size_t)ws);
+  if (base + hl.total - 4096 > (char*)ws + ws_bytes) return fail(FHTB_EINVAL, "workspace too small");
+  double* Cd = (double*)(base + hl.c_off);
+  double* Fd = (double*)(base + hl.f_off);
+  const long long ldc = g->n_data_cols, ldf = g->n_out;
+  const bool near = (flags & FHTB_NEAR) && !g->tiles.empty();
+  const bool far = (flags & FHTB_FAR) != 0;
+  double* Fn = (near && far) ? (double*)(base + hl.fn_off) : Fd;
+  cudaStream_t st = S(stream);
+  HostAux* hx;
+  if (int r = get_haux(st, &hx)) return r;
+  const int G = std::max(1, std::min({(int)n_groups, (int)n_vec, kMaxHostGroups}));
+  std::vector<int> v0(G + 1);
+  for (int i = 0; i <= G; ++i) v0[i] = (int)((long long)n_vec * i / G);
+  // requests sorted by vector, grouped
+  std::vector<int> perm(n_req);
+  for (int i = 0; i < n_req; ++i) perm[i] = i;
+  std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return reqs[a].vec < reqs[b].vec; });
+
+  // inputs, group by group, on the copy stream (after the caller's prior work)
+  CU(cudaEventRecord(hx->nstart, st));
+  CU(cudaStreamWaitEvent(hx->h2d, hx->nstart, 0));
+  for (int i = 0; i < G; ++i) {
+    const int nv = v0[i + 1] - v0[i];
+    CU(cudaMemcpy2DAsync(Cd + (size_t)v0[i] * ldc, ldc * sizeof(double), C_host + (size_t)v0[i] * ldc_host,
+                         ldc_host * sizeof(double), ldc * sizeof(double), nv, cudaMemcpyHostToDevice, hx->h2d));
+    CU(cudaEventRecord(hx->in[i], hx->h2d));
+  }
+  // near field of the whole batch on its own stream
+  if (near) {
+    CU(cudaStreamWaitEvent(hx->near, hx->in[G - 1], 0));
+    if (far) CU(cudaMemsetAsync(Fn, 0, sizeof(double) * (size_t)n_vec * ldf, hx->near));
+    else CU(cudaMemsetAsync(Fd, 0, sizeof(double) * (size_t)n_vec * ldf, hx->near));
+    if (int r = apply_impl(g, reqs, n_req, Cd, ldc, n_vec, Fn, ldf, FHTB_NEAR, 0, 1, nullptr, base + hl.near_off,
+                           hl.near_bytes, hx->near))
+      return r;
+    CU(cudaEventRecord(hx->ndone, hx->near));
+  }
+  std::vector<fhtb_request> sub;
+  size_t q = 0;
+  for (int i = 0; i < G; ++i) {
+    const int nv = v0[i + 1] - v0[i];
+    double* Fg = Fd + (size_t)v0[i] * ldf;
+    if (far) {
+      sub.clear();
+      while (q < perm.size() && reqs[perm[q]].vec < v0[i + 1]) {
+        fhtb_request r = reqs[perm[q]];
+        r.vec -= v0[i];
+        sub.push_back(r);
+        ++q;
+      }
+      CU(cudaStreamWaitEvent(st, hx->in[i], 0));
+      CU(cudaMemsetAsync(Fg, 0, sizeof(double) * (size_t)nv * ldf, st));
+      if (!sub.empty())
+        if (int r = apply_impl(g, sub.data(), (int)sub.size(), Cd + (size_t)v0[i] * ldc, ldc, nv, Fg, ldf, FHTB_FAR,
+                               0, 1, nullptr, base + hl.far_off, hl.far_bytes, st))
+          return r;
+    }
+    if (near) {
+      CU(cudaStreamWaitEvent(st, hx->ndone, 0));
+      if (far) CU(launch_add_rows(Fg, ldf, Fn + (size_t)v0[i] * ldf, ldf, nv, ldf, st));
+    } else if (!far) {
+      CU(cudaMemsetAsync(Fg, 0, sizeof(double) * (size_t)nv * ldf, st));
+    }
+    CU(cudaEventRecord(hx->fin[i], st));
+    CU(cudaStreamWaitEvent(hx->d2h, hx->fin[i], 0));
+    CU(cudaMemcpy2DAsync(F_host + (size_t)v0[i] * ldf_host, ldf_host * sizeof(double), Fg, ldf * sizeof(double),
+                         ldf * sizeof(double), nv, cudaMemcpyDeviceToHost, hx->d2h));
+  }
+  // the caller's stream completes after the last output copy
+  CU(cudaEventRecord(hx->fin[0], hx->d2h));
+  CU(cudaStreamWaitEvent(st, hx->fin[0], 0));
+  return FHTB_OK;
+}
+
+}  // extern "C"
+
 namespace {
 
 // Full (dmode 0) far-field units by the distributed four-step: per round of

@@ -187,6 +187,25 @@ class _Grid:
         del keep
         return F
 
+    HOST_GROUP_VECS = 8          # vectors per copy/compute group of apply_host
+
+    def apply_host(self, requests, C, F, flags=_lib.FHTB_FAR | _lib.FHTB_NEAR, n_groups=None):
+        """F = application of the requests, C and F pinned host float64
+        tensors (B, n_data_cols) / (B, n_out): fhtb_apply_host, the copies
+        overlapped with the far field in vector groups.  Same bits as
+        apply() on device copies with F = 0."""
+        if n_groups is None:
+            n_groups = max(1, -(-C.shape[0] // self.HOST_GROUP_VECS))
+        arr, keep = _pack_requests(requests)
+        ws_n = self._lib.fhtb_apply_host_workspace(self.handle, len(requests), C.shape[0], flags)
+        ws = _device.workspace(ws_n)
+        _lib.check(self._lib.fhtb_apply_host(self.handle, arr, len(requests), C.data_ptr(), C.stride(0),
+                                             C.shape[0], F.data_ptr(), F.stride(0), flags, int(n_groups),
+                                             _device.ptr(ws), ws.numel(), _device.stream_ptr()))
+        torch.cuda.current_stream().synchronize()
+        del keep
+        return F
+
     X_BUDGET = 1 << 30          # bytes per exchange buffer (send; recv the same)
 
     def _apply_exchange(self, arr, n_req, C, F, flags, s, n, xfn, unit, keep):
@@ -271,8 +290,30 @@ def _bump(stats, key, amount):
         stats[key] = stats.get(key, 0) + amount
 
 
+def _host_pinned_real(c):
+    """A pinned real float64 CPU tensor (vector or batch) takes the
+    host-buffer path (fhtb_apply_host) unless a work split is active."""
+    return (isinstance(c, torch.Tensor) and c.device.type == "cpu" and c.dtype == torch.float64
+            and c.ndim in (1, 2) and c.is_contiguous() and c.is_pinned() and _device.shard()[1] == 1)
+
+
 def _run(params, scheme, order_weights, c, stats, flags=_lib.FHTB_FAR | _lib.FHTB_NEAR):
     """Apply the partitioned scheme to c (vector, batch or tensor)."""
+    if _host_pinned_real(c):
+        if c.shape[-1] != params.n:
+            raise ValueError("coefficient length does not match params.n")
+        _device.ensure_init()
+        orders = sorted({int(o) for o, _ in order_weights})
+        g = _grid(params.n, params.gamma, params.m_terms, scheme.blocks, scheme.mask_segments, orders)
+        C = c.reshape(-1, c.shape[-1]).contiguous()
+        F = torch.empty(C.shape, dtype=torch.float64, pin_memory=True)
+        reqs = [dict(vec=v, terms=list(order_weights)) for v in range(C.shape[0])]
+        g.apply_host(reqs, C, F, flags)
+        if flags & _lib.FHTB_FAR:
+            _bump(stats, "transform_applications", C.shape[0] * 2 * params.m_terms * len(scheme.blocks))
+        if flags & _lib.FHTB_NEAR:
+            _bump(stats, "pointwise_evaluations", C.shape[0] * scheme.mask_size() * len(order_weights))
+        return F[0] if c.ndim == 1 else F
     C, meta = _device.as_real_batch(c)
     if C.shape[-1] != params.n:
         raise ValueError("coefficient length does not match params.n")

@@ -95,3 +95,31 @@ def test_dht_cfg4_fullsize_vs_direct(cuda_dev):
     tol = 10 * eps * C.abs().sum(1)
     assert bool((err <= tol).all()), (err.cpu().numpy(), tol.cpu().numpy())
     assert torch.equal(fh.dht(plan, C), F)
+
+
+@pytest.mark.parametrize("n,nu,gamma,eps,batch", [(2 ** 16, 0, 0.0, 1e-15, 19), (2 ** 20, 4, 4.0, 1e-15, 10),
+                                                  (3000, 2, 0.5, 1e-8, 5)])
+def test_host_buffer_path_bitwise(cuda_dev, n, nu, gamma, eps, batch):
+    """fhtb_apply_host (pinned host in and out, copies overlapped with the
+    far field in vector groups) gives the bits of the device-resident call,
+    for every grouping, and for far-only / near-only applications."""
+    from paper_1501_01652_b200 import _lib
+    from paper_1501_01652_b200.schlomilch import _grid
+    C = _cfg2_inputs(n, batch, 5)
+    params = fh.select_params(nu, n, eps, gamma=gamma)
+    ref = fh.schlomilch_fast(params, C).cpu()
+    pinned = C.cpu().pin_memory()
+    got = fh.schlomilch_fast(params, pinned)
+    assert got.device.type == "cpu" and got.is_pinned()
+    assert torch.equal(got, ref)
+    assert torch.equal(fh.schlomilch_fast(params, pinned[2].clone().pin_memory()), ref[2])
+    sc = fh.build_partition(params)
+    g = _grid(params.n, params.gamma, params.m_terms, sc.blocks, sc.mask_segments, [nu])
+    reqs = [dict(vec=v, terms=[(nu, 1.0)]) for v in range(batch)]
+    for flags in (_lib.FHTB_FAR, _lib.FHTB_NEAR, _lib.FHTB_FAR | _lib.FHTB_NEAR):
+        Fd = torch.zeros_like(C)
+        g.apply(reqs, C, Fd, flags)
+        for groups in (1, 3, batch):
+            Fh = torch.full(C.shape, np.nan, dtype=torch.float64).pin_memory()
+            g.apply_host(reqs, pinned, Fh, flags, n_groups=groups)
+            assert torch.equal(Fh, Fd.cpu()), (flags, groups)
