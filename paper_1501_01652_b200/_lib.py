@@ -11,7 +11,9 @@ import threading
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libfhtb200.so")
+# FHTB_LIB: an alternative build of the same library (A/B timing of kernel
+# changes inside one GPU session, tools/ab_build.sh); default the in-tree one
+LIB_PATH = os.environ.get("FHTB_LIB") or os.path.join(_PKG, "libfhtb200.so")
 
 FHTB_OK, FHTB_EINVAL, FHTB_ECUDA, FHTB_ENONFINITE, FHTB_ECONVERGE = 0, 1, 2, 3, 4
 FHTB_DCT1, FHTB_DST1 = 0, 1
@@ -102,7 +104,8 @@ def load(path=LIB_PATH):
                              ("FHTB_FAR_CHUNK_BYTES", b"far_chunk_bytes"),
                              ("FHTB_NEAR_CHUNK_COLS", b"near_chunk_cols"), ("FHTB_NEAR_SPLIT", b"near_split"), ("FHTB_FAR_STREAMS", b"far_streams"),
                              ("FHTB_NEAR_OVERLAP", b"near_overlap"),
-                             ("FHTB_FAR_PRUNE_ROWS", b"far_prune_rows")):
+                             ("FHTB_FAR_PRUNE_ROWS", b"far_prune_rows"), ("FHTB_FAR_MIN_COLS", b"far_min_cols"),
+                             ("FHTB_FAR_ROWDOT_BINS", b"far_rowdot_bins")):
                 if os.environ.get(env):
                     lib.fhtb_set_option(key, int(os.environ[env]))
             _lib = lib

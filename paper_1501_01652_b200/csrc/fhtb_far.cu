@@ -59,6 +59,7 @@ __device__ __forceinline__ void load_col(const FarArgs& a, const ReqDesc& R, lon
     double x = a.C[(long long)R.vec * a.ldc + (n - 1)];
     if (R.preA) x *= ipow_f(R.preA[n - 1], R.pa);
     if (R.preB) x *= ipow_f(R.preB[n - 1], R.pb);
+    // (computing beats loading w0_tab/iw_tab here: pass 1 28.1 vs 29.6 ms, cfg2)
     const double om = ((double)n + a.gamma) * 3.141592653589793;
     iw = 1.0 / om;
     v = x * (1.0 / sqrt(om));
@@ -246,6 +247,8 @@ far_pass1p_kernel(FarArgs a) {
 // r_0 and the MODE-2 column-shift phase phi_k are applied once at the end.
 // MODE 3: MODE 0 in exchange mode (distributed four-step): column pairs from
 //         a.xc0, rows assembled from the received chunks of all ranks.
+#define TQS_SMEM(MODE, E) ((MODE) == 2 && (E) >= 16)
+#define IRS_K(E, MODE) false
 template <int N1, int E, int MODE, int MINB>
 __global__ void __launch_bounds__((MODE == 1 ? 1 : 2) * (N1 / E), MINB)
 far_pass2_kernel(FarArgs a) {
@@ -272,12 +275,21 @@ far_pass2_kernel(FarArgs a) {
   const BlockDesc& B = a.blocks[U.block];
   const double2* tw = a.tw + (N1 - 2);
   const int xj = XCH ? __ldg(a.xrow + myk2).y : 0;
+  // L2 = Q / N1 is a power of two: k / L2 as a shift (a runtime division
+  // costs ~20 integer instructions per output and pair)
+  const int lgL2 = a.logQ - ilog2c(N1);
 
   // E <= 8: the shared-memory offsets of Z[k] and Z[2L-k] are kept per slot
   // (registers allow it); E = 16 recomputes them per pair
   constexpr bool PRE = (E <= 8 && N1 >= 1024);
-  int kq[NQ], oz[PRE ? NQ : 1], op[PRE ? NQ : 1];
-  double ir[NQ], rp[HOR ? 1 : NQ];
+  int kq[IRS_K(E, MODE) ? 1 : NQ], oz[PRE ? NQ : 1], op[PRE ? NQ : 1];
+  // IRS (E = 16, Horner modes): the row factors L/k live in shared memory
+  // ([q][tid] after the FFT buffers) instead of NQ registers, which the
+  // 16-point state cannot spare without spilling
+  constexpr bool IRS = false;   // (measured: 18.05 -> 18.30 ms at 2048 points, so off)
+  double* irs = reinterpret_cast<double*>(sm2 + NCOL * NP + (TQS_SMEM(MODE, E) ? NCOL * E : 0));
+  int* kqs = reinterpret_cast<int*>(irs + (IRS ? NQ * NT : 0));      // IRS: row indices too
+  double ir[IRS ? 1 : NQ], rp[HOR ? 1 : NQ];
   double2 acc[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
@@ -290,44 +302,58 @@ far_pass2_kernel(FarArgs a) {
       k = k2 + L2 * k1;
       if (k < 1 || k > L || k < B.r0 || k >= B.r1) k = 0;
     }
-    kq[q] = k;
+    if (IRS) kqs[q * NT + tid] = k;
+    else kq[IRS ? 0 : q] = k;
     acc[q] = make_double2(0.0, 0.0);
-    ir[q] = k ? a.Ld / (double)k : 0.0;
+    const double irq = k ? a.Ld / (double)k : 0.0;
+    if (IRS) irs[q * NT + tid] = irq;
+    else ir[IRS ? 0 : q] = irq;
     if (PRE) {
       const int kp = 2 * L - k;
-      oz[PRE ? q : 0] = k ? (((k & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(k / L2) : 0;
-      op[PRE ? q : 0] = k ? (((kp & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(kp / L2) : 0;
+      oz[PRE ? q : 0] = k ? (((k & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(k >> lgL2) : 0;
+      op[PRE ? q : 0] = k ? (((kp & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(kp >> lgL2) : 0;
     }
     if (!HOR) {
       double post = 1.0;
       if (k && R.pr) post = ipow_f((double)k / a.Ld, R.pr);
       if (k && R.post_e && R.pe) post *= ipow_f(R.post_e[k - 1], R.pe);
-      rp[HOR ? 0 : q] = k ? 0.5 * post * sqrt(ir[q]) : 0.0;
+      rp[HOR ? 0 : q] = k ? 0.5 * post * sqrt(irq) : 0.0;
     }
   }
   // column sources
   //   MODE 1: v = x omega^{-1/2}, iw = 1/omega kept per element (z = v (1, iw),
   //           v *= iw^2 per pair)
   //   MODE 2: tq = e^{2 pi i m k2/Q} per element; z = u_p[m] tq
+  //   MODE 2, E >= 16 (TQS): tq = tb * st[e], tb = e^{2 pi i tt k2/Q} per
+  //           thread and st[e] = e^{2 pi i T e k2/Q} per column in shared
+  //           memory (broadcast reads): E complex registers fewer, which
+  //           lets the column FFT run with E = 16 (one radix pass fewer)
+  constexpr bool TQS = (MODE == 2 && E >= 16);
   double v[ONEPASS ? E : 1], iw[ONEPASS ? E : 1];
-  double2 tq[MODE == 2 ? E : 1];
+  double2 tq[(MODE == 2 && !TQS) ? E : 1];
+  double2 tb = make_double2(1.0, 0.0);
   if (ONEPASS) {
     long long cA, cB;
     unit_cols(a, R, B, cA, cB);
 #pragma unroll
     for (int e = 0; e < E; ++e) load_col(a, R, cA, cB, tt + T * e, v[ONEPASS ? e : 0], iw[ONEPASS ? e : 0]);
   }
-  if (MODE == 2) {
+  if (MODE == 2 && TQS) {
+    double2* st = sm2 + NCOL * NP + h * E;
+    if (tt < E) st[tt] = myk2 ? qtw(a, (long long)T * tt * myk2) : make_double2(1.0, 0.0);
+    tb = myk2 ? qtw(a, (long long)tt * myk2) : make_double2(1.0, 0.0);
+    __syncthreads();
+  } else if (MODE == 2) {
 #pragma unroll
     for (int e = 0; e < E; ++e)
-      tq[MODE == 2 ? e : 0] = myk2 ? qtw(a, (long long)(tt + T * e) * myk2) : make_double2(1.0, 0.0);
+      tq[(MODE == 2 && !TQS) ? e : 0] = myk2 ? qtw(a, (long long)(tt + T * e) * myk2) : make_double2(1.0, 0.0);
   }
   if (!HOR) {
     for (int p = 0; p < a.p0; ++p) {        // advance to the shard's first pair
 #pragma unroll
       for (int e = 0; e < E; ++e) v[ONEPASS ? e : 0] = (v[ONEPASS ? e : 0] * iw[ONEPASS ? e : 0]) * iw[ONEPASS ? e : 0];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) rp[HOR ? 0 : q] = (rp[HOR ? 0 : q] * ir[q]) * ir[q];
+      for (int q = 0; q < NQ; ++q) rp[HOR ? 0 : q] = (rp[HOR ? 0 : q] * ir[IRS ? 0 : q]) * ir[IRS ? 0 : q];
     }
   }
   for (int pi = 0; pi < a.p1 - a.p0; ++pi) {
@@ -342,8 +368,14 @@ far_pass2_kernel(FarArgs a) {
       }
     } else if (MODE == 2) {
       const double2* u = a.G + (long long)(ul * a.M + p) * N1;
+      if (TQS) {
+        const double2* st = sm2 + NCOL * NP + h * E;
 #pragma unroll
-      for (int e = 0; e < E; ++e) z[e] = cmul(u[tt + T * e], tq[MODE == 2 ? e : 0]);
+        for (int e = 0; e < E; ++e) z[e] = cmul(cmul(u[tt + T * e], tb), st[e]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) z[e] = cmul(u[tt + T * e], tq[(MODE == 2 && !TQS) ? e : 0]);
+      }
     } else if (XCH) {
       // row myk2 assembled from the chunks of all source ranks
       const long long row = ((long long)(ul * a.M + p) * a.xrows + xj) << a.xlog;
@@ -358,22 +390,32 @@ far_pass2_kernel(FarArgs a) {
 #pragma unroll
       for (int e = 0; e < E; ++e) z[e] = G[tt + T * e];
     }
+    // E <= 8: the pair's row coefficients are loaded before the transform
+    // (their latency hides behind it); E = 16 has no registers to spare
+    // (measured: pass 2 at 2048 points 16.9 -> 18.3 ms with the early loads)
+    const int i0 = 2 * p, i1 = 2 * p + 1;
+    double ac0, bc0, ac1, bc1;
+    if (E <= 8) {
+      ac0 = R.ac[i0], bc0 = R.bc[i0];
+      ac1 = R.ac[i1], bc1 = R.bc[i1];
+    }
     __syncthreads();
     block_fft<N1, E, 1>(z, sm2 + h * NP, tt, tw);
     __syncthreads();
 #pragma unroll
     for (int s = 0; s < E; ++s) sm2[h * NP + swz<LOGE>(fft_out_index<N1, E>(tt, s))] = z[s];
     __syncthreads();
-    const int i0 = 2 * p, i1 = 2 * p + 1;
-    const double ac0 = R.ac[i0], bc0 = R.bc[i0];
-    const double ac1 = R.ac[i1], bc1 = R.bc[i1];
+    if (E > 8) {
+      ac0 = R.ac[i0], bc0 = R.bc[i0];
+      ac1 = R.ac[i1], bc1 = R.bc[i1];
+    }
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      const int k = kq[q];
+      const int k = IRS ? kqs[q * NT + tid] : kq[IRS ? 0 : q];
       if (!k) continue;
       const int kp = 2 * L - k;
-      const double2 Zk = sm2[PRE ? oz[PRE ? q : 0] : (((k & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(k / L2)];
-      const double2 Zp = cconj(sm2[PRE ? op[PRE ? q : 0] : (((kp & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(kp / L2)]);
+      const double2 Zk = sm2[PRE ? oz[PRE ? q : 0] : (((k & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(k >> lgL2)];
+      const double2 Zp = cconj(sm2[PRE ? op[PRE ? q : 0] : (((kp & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(kp >> lgL2)]);
       // 2 Ya, 2 Yb (the factor 1/2 is folded into r_0)
       double2 Ya = make_double2(Zk.x + Zp.x, Zk.y + Zp.y);
       double2 Yb = make_double2(Zk.y - Zp.y, Zp.x - Zk.x);
@@ -381,7 +423,7 @@ far_pass2_kernel(FarArgs a) {
       // t0 = (a0 - i b0) Ya, t1 = (a1 - i b1) Yb
       const double t0x = fma(ac0, Ya.x, bc0 * Ya.y), t0y = fma(ac0, Ya.y, -bc0 * Ya.x);
       const double t1x = fma(ac1, Yb.x, bc1 * Yb.y), t1y = fma(ac1, Yb.y, -bc1 * Yb.x);
-      const double w = ir[q];
+      const double w = IRS ? irs[q * NT + tid] : ir[IRS ? 0 : q];
       if (HOR) {
         const double w2 = w * w;
         acc[q].x = fma(acc[q].x, w2, fma(w, t1x, t0x));
@@ -403,21 +445,22 @@ far_pass2_kernel(FarArgs a) {
   double* part = a.part + (long long)ul * a.part_stride;
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
-    const int k = kq[q];
+    const int k = IRS ? kqs[q * NT + tid] : kq[IRS ? 0 : q];
     if (!k) continue;
     double2 u = acc[q];
     if (HOR) {
       double post = 1.0;
       if (R.pr) post = ipow_f((double)k / a.Ld, R.pr);
       if (R.post_e && R.pe) post *= ipow_f(R.post_e[k - 1], R.pe);
-      double r0 = 0.5 * post * sqrt(ir[q]);
-      for (int p = 0; p < a.p0; ++p) r0 = (r0 * ir[q]) * ir[q];    // (L/k)^{2 p0}
+      const double irq = IRS ? irs[q * NT + tid] : ir[IRS ? 0 : q];
+      double r0 = 0.5 * post * sqrt(irq);
+      for (int p = 0; p < a.p0; ++p) r0 = (r0 * irq) * irq;    // (L/k)^{2 p0}
       u = make_double2(u.x * r0, u.y * r0);
     }
     if (MODE == 2 && sh) {
       // phi_k = e^{i pi k sh / L}; exactly (-1)^sh at k = L
       const double2 phi = (k == L) ? make_double2((sh & 1) ? -1.0 : 1.0, 0.0)
-                                   : qtw(a, ((long long)k * sh) % (2 * a.L));
+                                   : qtw(a, ((long long)k * sh) & (2 * a.L - 1));   // 2L = Q, a power of two
       u = cmul(u, phi);
     }
     double val = u.x;
@@ -452,18 +495,134 @@ __global__ void colgen_prep_kernel(FarArgs a) {
   }
 }
 
-// Pass 2 of a block whose rows all lie below L2 (narrow-row side block): only
-// k1 = 0 (and the partner k1 = L1-1) of each column FFT is needed, i.e. two
-// weighted sums over n1 per column instead of an L1-point FFT:
-//   Z[k2]           = sum_n1 G[k2][n1]
-//   Z[2L - (L2-k2)] = sum_n1 G[k2][n1] e^{-2 pi i n1 / L1}
+// Pass 2 of a block whose rows all lie below K*L2 (narrow-row side block):
+// only the FFT bins k1 < K of each column (and their partners near L1) are
+// needed, i.e. 2K weighted sums over n1 per column instead of an L1-point FFT:
+//   Z[c + L2 j]       = sum_n1 G[c][n1] e^{+2 pi i n1 j / L1}        (j < K)
+//   Z[2L - (c + L2 j)] = sum_n1 G[L2-c][n1] e^{-2 pi i n1 (j+1) / L1}  (c != 0)
+//                      = sum_n1 G[0][n1] e^{-2 pi i n1 j / L1}       (c == 0)
 // CTA = (column pair {c, L2-c}, unit); warps 0-3 sum column c, warps 4-7
 // column L2-c, each over a quarter of n1, for all pairs first (loads of all
-// pairs in flight together), then two threads combine the quarters in fixed
+// pairs in flight together), then 2K threads combine the quarters in fixed
 // order and run the epilogue (same algebra as far_pass2_kernel).
+// KB: compile-time bound on the bins of the chunk's units (1, 2 or 4).
+// Measured on cfg2: the 3-bin form of the block with rows [539, 2488)
+// (15.4 ms per 64 vectors) loses to its full pass 2 (8.4 ms), so the
+// default keeps one bin per column (far_rowdot_bins = 1).
 constexpr int kMaxPairs = 16;
+template <int KB>
 __global__ void __launch_bounds__(256)
 far_rowdot_kernel(FarArgs a, int c_lo) {
+  constexpr int kMaxBins = KB;
+  const int L = (int)a.L;
+  const int L1 = a.L1, L2 = a.L2;
+  const int c = c_lo + blockIdx.x;
+  const int ul = blockIdx.y;
+  const UnitDesc U = a.units[a.u0 + ul];
+  const ReqDesc& R = a.reqs[U.req];
+  const BlockDesc& B = a.blocks[U.block];
+  // all KB bins are summed (compile-time trip counts keep the loads of the
+  // unrolled n1 loop in flight together); bins past the block rows are not
+  // written
+  constexpr int K = KB;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int cb = (L2 - c) % L2;
+  // outputs k = c + L2 j and k = cb + L2 j (cb != c), j < K, inside the block
+  bool any = false;
+  for (int j = 0; j < K; ++j) {
+    const int kA = c + L2 * j, kB = cb + L2 * j;
+    any |= kA >= 1 && kA <= L && kA >= B.r0 && kA < B.r1;
+    any |= cb != c && kB >= 1 && kB <= L && kB >= B.r0 && kB < B.r1;
+  }
+  if (!any) return;
+  __shared__ double2 part_s[8][kMaxPairs][2 * kMaxBins];
+  const int side_w = wid >> 2, quarter = wid & 3;
+  const int col = side_w == 0 ? c : cb;
+  const double2* rot = a.tw + (L1 - 2);   // e^{+2 pi i m / L1}
+  const int msk = L1 - 1;
+  const int qlen = (L1 + 3) / 4;
+  const int lo = quarter * qlen, hi = min(L1, lo + qlen);
+  for (int p = a.p0; p < a.p1; ++p) {
+    const double2* g = a.G + ((long long)(ul * a.M + p) * L2 + col) * L1;
+    double2 sp[kMaxBins], sn[kMaxBins];
+#pragma unroll
+    for (int j = 0; j < kMaxBins; ++j) sp[j] = sn[j] = make_double2(0.0, 0.0);
+#pragma unroll 4
+    for (int n1 = lo + lane; n1 < hi; n1 += 32) {
+      const double2 v = g[n1];
+      sp[0] = cadd(sp[0], v);
+#pragma unroll
+      for (int j = 1; j <= kMaxBins; ++j) {
+        const double2 t = __ldg(rot + ((n1 * j) & msk));
+        if (j < K) sp[j] = cadd(sp[j], cmul(v, t));
+        sn[j - 1] = cadd(sn[j - 1], cmul(v, cconj(t)));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxBins; ++j) {
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        sp[j].x += __shfl_xor_sync(0xffffffffu, sp[j].x, off);
+        sp[j].y += __shfl_xor_sync(0xffffffffu, sp[j].y, off);
+        sn[j].x += __shfl_xor_sync(0xffffffffu, sn[j].x, off);
+        sn[j].y += __shfl_xor_sync(0xffffffffu, sn[j].y, off);
+      }
+      if (lane == 0) {
+        part_s[wid][p][j] = sp[j];
+        part_s[wid][p][kMaxBins + j] = sn[j];
+      }
+    }
+  }
+  __syncthreads();
+  const int side = threadIdx.x / K, j = threadIdx.x % K;
+  if (side >= 2) return;
+  if (side == 1 && cb == c) return;
+  const int kcol = side == 0 ? c : cb;
+  const int k = kcol + L2 * j;
+  if (!(k >= 1 && k <= L && k >= B.r0 && k < B.r1)) return;
+  // Z[k] from this side's column; conj Z[2L-k] from the partner column
+  // (itself when cb == c) at the minus sum j+1, or column 0's own minus sum j
+  const int sk = side, spn = side ^ (cb != c ? 1 : 0);
+  const int zi = (kcol == 0) ? kMaxBins + j - 1 : kMaxBins + j;
+  const double ir = a.Ld / (double)k;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int p = a.p1 - 1; p >= a.p0; --p) {
+    double2 Zk = part_s[4 * sk][p][j], Zp = part_s[4 * spn][p][zi];
+#pragma unroll
+    for (int w = 1; w < 4; ++w) {
+      Zk = cadd(Zk, part_s[4 * sk + w][p][j]);
+      Zp = cadd(Zp, part_s[4 * spn + w][p][zi]);
+    }
+    Zp = cconj(Zp);
+    double2 Ya = make_double2(Zk.x + Zp.x, Zk.y + Zp.y);
+    double2 Yb = make_double2(Zk.y - Zp.y, Zp.x - Zk.x);
+    if (k == L) { Ya.y = 0.0; Yb.y = 0.0; }
+    const int i0 = 2 * p, i1 = 2 * p + 1;
+    const double ac0 = R.ac[i0], bc0 = R.bc[i0], ac1 = R.ac[i1], bc1 = R.bc[i1];
+    const double t0x = fma(ac0, Ya.x, bc0 * Ya.y), t0y = fma(ac0, Ya.y, -bc0 * Ya.x);
+    const double t1x = fma(ac1, Yb.x, bc1 * Yb.y), t1y = fma(ac1, Yb.y, -bc1 * Yb.x);
+    const double w2 = ir * ir;
+    acc.x = fma(acc.x, w2, fma(ir, t1x, t0x));
+    acc.y = fma(acc.y, w2, fma(ir, t1y, t0y));
+  }
+  double post = 1.0;
+  if (R.pr) post = ipow_f((double)k / a.Ld, R.pr);
+  if (R.post_e && R.pe) post *= ipow_f(R.post_e[k - 1], R.pe);
+  double r0 = 0.5 * post * sqrt(ir);
+  for (int p = 0; p < a.p0; ++p) r0 = (r0 * ir) * ir;           // (L/k)^{2 p0}
+  double v = acc.x * r0;
+  if (a.cs_tab) {
+    const double2 th = __ldg(a.cs_tab + (k - 1));
+    v = v * th.x + (acc.y * r0) * th.y;
+  }
+  a.part[(long long)ul * a.part_stride + (k - 1)] = v;
+}
+
+// One bin per column (the default narrow-row form): the single-bin kernel
+// keeps both loads of four unrolled iterations in flight (the general
+// far_rowdot_kernel<1> measured 5.9 vs 3.9 ms on cfg2).
+__global__ void __launch_bounds__(256)
+far_rowdot1_kernel(FarArgs a, int c_lo) {
   const int L = (int)a.L;
   const int L1 = a.L1, L2 = a.L2;
   const int c = c_lo + blockIdx.x;
@@ -705,9 +864,9 @@ __global__ void far_reduce_kernel(FarArgs a, int n_units) {
 
 // ---------------------------------------------------------------- launch
 // bits 0-3: pass-1 shape at 1024; 4-7: pass-2 shape at 2048; 8-11: paired-lane
-// pass 2; 12-15: per-pair pass 1.  Default = best measured on B200 (sweeps in
-// profiles/round1_far_variants.md).
-int g_far_variant = 20;
+// pass 2; 12-15: per-pair pass 1; bit 16: no TMA stores; 20-23: narrow-column
+// FFT shape.  Default = best measured on B200.
+int g_far_variant = 20 + (1 << 20);
 
 // 2D tensor map over G viewed as rows of 2*L1 doubles (one row per (unit,
 // pair, k2)); cuTensorMapEncodeTiled is fetched through the runtime so the
@@ -773,7 +932,8 @@ template <int N1, int E, int MODE, int MINB>
 static cudaError_t p2_t(const FarArgs& a, int gx, int gy, cudaStream_t st) {
   constexpr int T = N1 / E;
   constexpr int NCOL = MODE == 1 ? 1 : 2;
-  const int smem = NCOL * (N1 + 4) * 16;
+  const int smem = (NCOL * (N1 + 4) + (TQS_SMEM(MODE, E) ? NCOL * E : 0)) * 16 +
+                   (IRS_K(E, MODE) ? (E / 2) * NCOL * T * 12 : 0);   // + IRS row factors, rows
   auto k = far_pass2_kernel<N1, E, MODE, MINB>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -788,6 +948,17 @@ static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
       case 2: return p2_t<N1, 8, MODE, 1>(a, gx, gy, st);
       case 3: return p2_t<N1, 16, MODE, 1>(a, gx, gy, st);
       case 4: return p2_t<N1, 8, MODE, 2>(a, gx, gy, st);
+      default: break;
+    }
+  }
+  // narrow-column blocks: bits 20-23 of the variant pick E = 16 with the
+  // shared step-table twiddles (TQS) for the column FFT
+  if constexpr (MODE == 2 && N1 >= 512) {
+    switch ((g_far_variant >> 20) & 15) {
+      // measured (cfg2, 64 vectors): 2048 columns 11.7 -> 10.4 ms with E = 16;
+      // 512 columns 14.6 -> 15.6 ms, so they keep E = 8 under case 1
+      case 1: if (N1 >= 1024) return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : 3)>(a, gx, gy, st); break;
+      case 2: return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : N1 >= 1024 ? 3 : 6)>(a, gx, gy, st);
       default: break;
     }
   }
@@ -822,8 +993,12 @@ cudaError_t launch_far_colgen(const FarArgs& a, int logN1, int n_units, cudaStre
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_far_rowdot(const FarArgs& a, int n_units, cudaStream_t st) {
-  note_launch(), far_rowdot_kernel<<<dim3(a.L2 / 2 + 1, n_units), 256, 0, st>>>(a, 0);
+cudaError_t launch_far_rowdot(const FarArgs& a, int n_units, int kbins, cudaStream_t st) {
+  const dim3 grid(a.L2 / 2 + 1, n_units);
+  if (kbins <= 1) note_launch(), far_rowdot1_kernel<<<grid, 256, 0, st>>>(a, 0);
+  else if (kbins <= 2) note_launch(), far_rowdot_kernel<2><<<grid, 256, 0, st>>>(a, 0);
+  else if (kbins <= 3) note_launch(), far_rowdot_kernel<3><<<grid, 256, 0, st>>>(a, 0);
+  else note_launch(), far_rowdot_kernel<4><<<grid, 256, 0, st>>>(a, 0);
   return cudaGetLastError();
 }
 

@@ -36,6 +36,8 @@ int g_near_split = 1;                      // near field: order-parity classes
 int g_far_streams = 2;                     // far-field chunks in flight (direct two-pass)
 int g_near_overlap = 1;                    // near field on its own stream beside the far field
 int g_prune_rows = 11;                     // narrow-row blocks: rows below 2^g_prune_rows
+int g_rowdot_bins = 1;                     // narrow-row blocks: at most this many pass-2 bins per column
+int g_min_lc = 9;                          // narrow-column blocks: smallest column FFT 2^g_min_lc
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -486,6 +488,16 @@ int fhtb_set_option(const char* key, int64_t value) {
     g_far_prune = (int)value;
     return FHTB_OK;
   }
+  if (!std::strcmp(key, "far_rowdot_bins")) {
+    if (value < 1 || value > 4) return fail(FHTB_EINVAL, "far_rowdot_bins must be 1..4");
+    g_rowdot_bins = (int)value;
+    return FHTB_OK;
+  }
+  if (!std::strcmp(key, "far_min_cols")) {
+    if (value < 7 || value > 12) return fail(FHTB_EINVAL, "far_min_cols must be 7..12");
+    g_min_lc = (int)value;
+    return FHTB_OK;
+  }
   if (!std::strcmp(key, "far_prune_rows")) {
     if (value < 10 || value > 12) return fail(FHTB_EINVAL, "far_prune_rows must be 10..12");
     g_prune_rows = (int)value;
@@ -674,15 +686,24 @@ int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
       x.dlogL1 = g->logN1;
       const long long cend = std::min(x.c1, g->n_data_cols + 1);   // columns n < cend
       // narrow-column blocks are shifted to their first column (fhtb_far.cu MODE 2)
-      const int lc = std::max(9, ilog2ll(std::max<long long>(cend - x.c0, 2)));
+      const int lc = std::max(g_min_lc, ilog2ll(std::max<long long>(cend - x.c0, 2)));
       // L2 >= r1 so that every block row has k1 = 0; keep L2 >= 1024 (the
       // pass-1 FFT is least efficient below that) and L1 <= 2048 (rowdot sums)
       const int lr = std::max(std::max(g->logQ - 11, 10), ilog2ll(std::max<long long>(x.r1, 2)));
+      // narrow rows with the pass-1 FFT kept at 2^lr0 points: the rows k < r1
+      // need the bins k1 <= (r1-1) >> lr0 of each column (2 sums per bin)
+      const int lr0 = std::max(g->logQ - 11, 10);
+      const long long kb = ((std::max<long long>(x.r1, 2) - 1) >> lr0) + 1;
+      x.kbins = 1;
       if (g_far_prune && lc <= 12 && lc < g->logQ) {
         x.dmode = 1;                 // narrow columns: pass 1 degenerates
         x.dlogL1 = lc;
+      } else if (g_far_prune && kb <= g_rowdot_bins && lr0 < g->logQ && g->logQ - lr0 <= 13) {
+        x.dmode = 2;                 // narrow rows: pass 2 collapses to 2*kbins sums
+        x.dlogL1 = g->logQ - lr0;
+        x.kbins = (int)kb;
       } else if (g_far_prune && lr <= g_prune_rows && lr < g->logQ && g->logQ - lr <= 13) {
-        x.dmode = 2;                 // narrow rows: pass 2 collapses to two sums
+        x.dmode = 2;                 // narrow rows with a longer pass-1 FFT, one bin
         x.dlogL1 = g->logQ - lr;
       }
     }
@@ -1472,7 +1493,10 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
               CU(launch_far_colgen(a, l1, n_units, cs));
             } else if (mode == 2) {
               CU(launch_far_pass1(a, l2, n_units, cs));
-              CU(launch_far_rowdot(a, n_units, cs));
+              int kb = 1;
+              for (int u = fp.chunks[ci].x; u < fp.chunks[ci].y; ++u)
+                kb = std::max(kb, g->bdesc[fp.units[u].block].kbins);
+              CU(launch_far_rowdot(a, n_units, kb, cs));
             } else {
               CU(launch_far_pass1(a, l2, n_units, cs));
               CU(launch_far_pass2(a, l1, n_units, cs));

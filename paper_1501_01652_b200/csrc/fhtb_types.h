@@ -43,6 +43,9 @@ struct BlockDesc {
   // 2 narrow rows (pass 2 = two sums per column)
   int dmode;
   int dlogL1;
+  // dmode 2: FFT bins k1 < kbins of each column are needed (rows k < kbins * L2)
+  int kbins;
+  int pad2_;
 };
 
 // Work unit of the far field: one request on one block.
