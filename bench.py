@@ -279,7 +279,8 @@ def run_ours(args):
                      "traffic": traffic_from_profile(), "model_bytes_per_vector": bpv,
                      "survey_model_bytes_per_vector": bpv_survey,
                      "survey_model_equivalent_gbs": bpv_survey * batch / (far_ms / 1e3) / 1e9,
-                     "peak_source": peak_src},
+                     "peak_source": peak_src,
+                     "limiter_evidence": bounds_from_profile()},
         "e2e": {"value": batch * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(host.nbytes),
                 "d2h_bytes_per_step": int(out.nbytes)},
         "gpu_launches": int(l1 - l0),
@@ -380,6 +381,24 @@ def run_tasks(fh, dev, rank, world, steps, warmup):
                                    "model_bytes_per_vector": bpv,
                                    "model_frac_of_hbm": bpv * B / (ms / 1e3) / 1e9 / peak}
     return out
+
+
+def bounds_from_profile():
+    """Limiter evidence of the dominant far kernels (ncu --set full,
+    tools/kernel_bounds.py): they run at ~75% of L1/TEX (shared-memory FFT
+    exchanges) with DRAM at 30-36%, so HBM is not what bounds them."""
+    p = os.path.join(ROOT, "profiles", "far_kernel_bounds.json")
+    try:
+        with open(p) as f:
+            seen, out = set(), []
+            for d in json.load(f)["launches"]:
+                if d["kernel"] in seen:
+                    continue
+                seen.add(d["kernel"])
+                out.append({k: d.get(k) for k in ("kernel", "l1tex_pct", "dram_pct", "issue_pct", "duration_us")})
+            return out
+    except Exception:
+        return None
 
 
 def traffic_from_profile():
