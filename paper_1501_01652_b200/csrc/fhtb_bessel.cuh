@@ -86,12 +86,34 @@ __device__ __forceinline__ double jn_miller(int nu, double z) {
     if (((k - 1) & 1) == 0) nrm += 2.0 * cur;
     --k;
   }
+  // the even order of every two-step trip has the same parity slot
+  const bool ev1 = ((k - 1) & 1) == 0;
+  double tk = 2.0 * k;                      // 2k, exact, counted down in doubles (no I2F per step)
+  // eight steps per trip with one overflow check while the growth of eight
+  // steps, at most (2 k0 / z)^8 < 1e48, stays inside the 1e58 headroom
+  if (tk * rz < 1e6) {
+    for (; k > nu + 8; k -= 8) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const double lo = fma(tk * rz, cur, -up);
+        const double lo2 = fma((tk - 2.0) * rz, lo, -cur);
+        nrm += 2.0 * (ev1 ? lo : lo2);
+        up = lo;
+        cur = lo2;
+        tk -= 4.0;
+      }
+      if (fabs(cur) > 1e250) {
+        cur *= 1e-250; up *= 1e-250; nrm *= 1e-250;
+      }
+    }
+  }
   for (; k > nu + 1; k -= 2) {
-    const double lo = fma((2.0 * k) * rz, cur, -up);
-    const double lo2 = fma((2.0 * (k - 1)) * rz, lo, -cur);
-    nrm += 2.0 * (((k - 1) & 1) == 0 ? lo : lo2);
+    const double lo = fma(tk * rz, cur, -up);
+    const double lo2 = fma((tk - 2.0) * rz, lo, -cur);
+    nrm += 2.0 * (ev1 ? lo : lo2);
     up = lo;
     cur = lo2;
+    tk -= 4.0;
     if (fabs(cur) > 1e250) {
       cur *= 1e-250; up *= 1e-250; nrm *= 1e-250;
     }
@@ -152,13 +174,33 @@ __device__ __forceinline__ void jn_all(int omax, double z, const JOrder* __restr
     if (((k - 1) & 1) == 0) nrm += 2.0 * cur;
     --k;
   }
+  // orders k-1 and k-2: exactly one of them is even, the same slot every trip
+  const bool ev1 = ((k - 1) & 1) == 0;
+  double tk = 2.0 * k;                      // 2k, exact (no I2F per step)
+  // eight steps per overflow check while (2 k0 / z)^8 < 1e48 (jn_miller)
+  if (tk * rz < 1e6) {
+    for (; k > OMAX + 7; k -= 8) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const double lo = fma(tk * rz, cur, -up);
+        const double lo2 = fma((tk - 2.0) * rz, lo, -cur);
+        nrm += 2.0 * (ev1 ? lo : lo2);
+        up = lo;
+        cur = lo2;
+        tk -= 4.0;
+      }
+      if (fabs(cur) > 1e250) {
+        cur *= 1e-250; up *= 1e-250; nrm *= 1e-250;
+      }
+    }
+  }
   for (; k > OMAX; k -= 2) {
-    double lo = fma((2.0 * k) * rz, cur, -up);
-    const double lo2 = fma((2.0 * (k - 1)) * rz, lo, -cur);
-    // orders k-1 and k-2: exactly one of them is even
-    nrm += 2.0 * (((k - 1) & 1) == 0 ? lo : lo2);
+    const double lo = fma(tk * rz, cur, -up);
+    const double lo2 = fma((tk - 2.0) * rz, lo, -cur);
+    nrm += 2.0 * (ev1 ? lo : lo2);
     up = lo;
     cur = lo2;
+    tk -= 4.0;
     if (fabs(cur) > 1e250) {
       cur *= 1e-250; up *= 1e-250; nrm *= 1e-250;
     }

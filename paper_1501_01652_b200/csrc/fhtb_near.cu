@@ -95,7 +95,27 @@ near_kernel(NearArgs a) {
   for (int f = 0; f < JT / 8; ++f) wmma::fill_fragment(acc[f], 0.0);
   const int nfrag = (nq + 7) >> 3;
 
+  constexpr int NBE = (NK * JT + kNearThreads - 1) / kNearThreads;   // Bs elements per thread
   for (long long n0 = tile.na; n0 < tile.nb; n0 += NK) {
+    // ---- coefficients of this step, loaded into registers first so their
+    // latency hides behind the Bessel tile (stored to Bs after it)
+    double xv[NBE];
+#pragma unroll
+    for (int t = 0; t < NBE; ++t) {
+      const int e = tid + t * kNearThreads;
+      const int q = e / JT, c = e % JT;
+      const long long n = n0 + q;
+      double x = 0.0;
+      if (e < NK * JT && c < nq && n < tile.nb) {
+        const ReqDesc* r = a.reqs + q0 + c;
+        if (n >= r->col_lo && n <= a.n_data_cols) {
+          x = a.C[(long long)r->vec * a.ldc + (n - 1)];
+          if (r->preA) x *= ipow(r->preA[n - 1], r->pa);
+          if (r->preB) x *= ipow(r->preB[n - 1], r->pb);
+        }
+      }
+      xv[t] = x;
+    }
     // ---- Bessel tile: As[i][u*NK + q] = J_{orders[u]}(z_{i,q})
     for (int e = tid; e < kRT * NK; e += kNearThreads) {
       const int i = e / NK, q = e % NK;
@@ -135,23 +155,17 @@ near_kernel(NearArgs a) {
       }
     }
     // ---- weighted coefficient tile: Bs[u*NK + q][c] = w_c[u] * x_c[n]
-    for (int e = tid; e < NK * JT; e += kNearThreads) {
+#pragma unroll
+    for (int t = 0; t < NBE; ++t) {
+      const int e = tid + t * kNearThreads;
+      if (e >= NK * JT) break;
       const int q = e / JT, c = e % JT;
       const long long n = n0 + q;
-      double x = 0.0;
-      const ReqDesc* r = nullptr;
-      if (c < nq && n < tile.nb) {
-        r = a.reqs + q0 + c;
-        if (n >= r->col_lo && n <= a.n_data_cols) {
-          x = a.C[(long long)r->vec * a.ldc + (n - 1)];
-          if (r->preA) x *= ipow(r->preA[n - 1], r->pa);
-          if (r->preB) x *= ipow(r->preB[n - 1], r->pb);
-        }
-      }
+      const ReqDesc* r = (c < nq && n < tile.nb) ? a.reqs + q0 + c : nullptr;
 #pragma unroll
       for (int u = 0; u < NORD; ++u) {
         const int pu = split ? ((u & 1) ? PE + (u >> 1) : (u >> 1)) : u;
-        Bs[(pu * NK + q) * JB + c] = r ? r->w[u] * x : 0.0;
+        Bs[(pu * NK + q) * JB + c] = r ? r->w[u] * xv[t] : 0.0;
       }
     }
     __syncthreads();
