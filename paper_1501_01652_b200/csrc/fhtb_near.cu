@@ -90,9 +90,20 @@ near_kernel(NearArgs a) {
     return;
   }
 
-  wmma::fragment<wmma::accumulator, 8, 8, 4, double> acc[JT / 8];
+  // 2D warp tiling of the kRT x JT output: WR x WC warps, each FR x FC
+  // fragments of 8 x 8, so that a warp loads FR A- and FC B-fragments per
+  // k-step for FR*FC DMMAs (8 rows x JT columns per warp loaded every B
+  // fragment once per row fragment: 1 + JT/8 loads for JT/8 DMMAs)
+  constexpr int WC = JT >= 128 ? 4 : 2;
+  constexpr int WR = (kNearThreads / 32) / WC;
+  constexpr int FR = (kRT / 8) / WR;
+  constexpr int FC = (JT / 8) / WC;
+  const int wr = warp / WC, wc = warp % WC;
+  wmma::fragment<wmma::accumulator, 8, 8, 4, double> acc[FR][FC];
 #pragma unroll
-  for (int f = 0; f < JT / 8; ++f) wmma::fill_fragment(acc[f], 0.0);
+  for (int r = 0; r < FR; ++r)
+#pragma unroll
+    for (int c = 0; c < FC; ++c) wmma::fill_fragment(acc[r][c], 0.0);
   const int nfrag = (nq + 7) >> 3;
 
   constexpr int NBE = (NK * JT + kNearThreads - 1) / kNearThreads;   // Bs elements per thread
@@ -169,20 +180,24 @@ near_kernel(NearArgs a) {
       }
     }
     __syncthreads();
-    // ---- DMMA: warp w owns rows [8w, 8w+8).  Fragment f of class 0 (even
-    // orders) contracts only k-steps < KE, class 1 (odd) only >= KE.
+    // ---- DMMA: warp (wr, wc) owns row fragments wr*FR.. and column
+    // fragments wc*FC..  Column fragment f of class 0 (even orders)
+    // contracts only k-steps < KE, class 1 (odd) only >= KE.
     constexpr int KE = (PE * NK) / 4;     // k-steps of the even-order half
 #pragma unroll
     for (int kk = 0; kk < K / 4; ++kk) {
-      wmma::fragment<wmma::matrix_a, 8, 8, 4, double, wmma::row_major> fa;
-      wmma::load_matrix_sync(fa, As + (warp * 8) * KA + kk * 4, KA);
+      wmma::fragment<wmma::matrix_a, 8, 8, 4, double, wmma::row_major> fa[FR];
 #pragma unroll
-      for (int f = 0; f < JT / 8; ++f) {
+      for (int r = 0; r < FR; ++r) wmma::load_matrix_sync(fa[r], As + ((wr * FR + r) * 8) * KA + kk * 4, KA);
+#pragma unroll
+      for (int c = 0; c < FC; ++c) {
+        const int f = wc * FC + c;
         const bool on = f < nfrag && (kk < KE ? f < fe || f >= fo : f >= fe);
         if (on) {
           wmma::fragment<wmma::matrix_b, 8, 8, 4, double, wmma::row_major> fb;
           wmma::load_matrix_sync(fb, Bs + (kk * 4) * JB + f * 8, JB);
-          wmma::mma_sync(acc[f], fa, fb, acc[f]);
+#pragma unroll
+          for (int r = 0; r < FR; ++r) wmma::mma_sync(acc[r][c], fa[r], fb, acc[r][c]);
         }
       }
     }
@@ -190,8 +205,10 @@ near_kernel(NearArgs a) {
   }
   // ---- epilogue: reduce request columns into vectors with post factors
 #pragma unroll
-  for (int f = 0; f < JT / 8; ++f)
-    wmma::store_matrix_sync(Cs + (warp * 8) * JB + f * 8, acc[f], JB, wmma::mem_row_major);
+  for (int r = 0; r < FR; ++r)
+#pragma unroll
+    for (int c = 0; c < FC; ++c)
+      wmma::store_matrix_sync(Cs + ((wr * FR + r) * 8) * JB + (wc * FC + c) * 8, acc[r][c], JB, wmma::mem_row_major);
   __syncthreads();
   const int v0 = a.grp_v0[g], v1 = a.grp_v0[g + 1];
   const int nv = v1 - v0;
