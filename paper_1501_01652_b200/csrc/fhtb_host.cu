@@ -405,6 +405,14 @@ void make_tiles(const std::vector<long long>& segs, long long first, long long s
       }
     }
   }
+  // launch order: most work first (longest-processing-time order), so the
+  // short tiles -- partial row tiles, last column chunks -- fill the tail of
+  // the grid instead of the long ones.  Results do not depend on the order:
+  // every tile owns its partial slot (or its rows), and the slots are
+  // reduced per row tile in chunk order.
+  std::stable_sort(tiles.begin(), tiles.end(), [](const NearTile& x, const NearTile& y) {
+    return (long long)x.nrows * (x.nb - x.na) > (long long)y.nrows * (y.nb - y.na);
+  });
 }
 
 }  // namespace
