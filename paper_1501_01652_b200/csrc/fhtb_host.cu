@@ -37,7 +37,8 @@ int g_far_streams = 2;                     // far-field chunks in flight (direct
 int g_near_overlap = 1;                    // near field on its own stream beside the far field
 int g_prune_rows = 11;                     // narrow-row blocks: rows below 2^g_prune_rows
 int g_rowdot_bins = 1;                     // narrow-row blocks: at most this many pass-2 bins per column
-int g_min_lc = 9;                          // narrow-column blocks: smallest column FFT 2^g_min_lc
+int g_min_lc = 9;
+int g_host_taper = 4;                      // fhtb_apply_host: inner/outer group size ratio                          // narrow-column blocks: smallest column FFT 2^g_min_lc
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -494,6 +495,11 @@ int fhtb_set_option(const char* key, int64_t value) {
   if (!key) return fail(FHTB_EINVAL, "null key");
   if (!std::strcmp(key, "far_prune")) {
     g_far_prune = (int)value;
+    return FHTB_OK;
+  }
+  if (!std::strcmp(key, "host_taper")) {
+    if (value < 1 || value > 64) return fail(FHTB_EINVAL, "host_taper must be 1..64");
+    g_host_taper = (int)value;
     return FHTB_OK;
   }
   if (!std::strcmp(key, "far_rowdot_bins")) {
@@ -1126,8 +1132,18 @@ int fhtb_apply_host(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req,
   HostAux* hx;
   if (int r = get_haux(st, &hx)) return r;
   const int G = std::max(1, std::min({(int)n_groups, (int)n_vec, kMaxHostGroups}));
+  // tapered groups: the first group's copy-in and the last group's copy-out
+  // are the exposed parts, so those two groups get 1/host_taper of the share
+  // of the inner ones (weights 1, t, ..., t, 1)
   std::vector<int> v0(G + 1);
-  for (int i = 0; i <= G; ++i) v0[i] = (int)((long long)n_vec * i / G);
+  {
+    std::vector<double> cw(G + 1, 0.0);
+    for (int i = 0; i < G; ++i) cw[i + 1] = cw[i] + ((G > 2 && (i == 0 || i == G - 1)) ? 1.0 : (double)g_host_taper);
+    for (int i = 0; i <= G; ++i) v0[i] = (int)std::llround(n_vec * cw[i] / cw[G]);
+    v0[G] = n_vec;
+    for (int i = G - 1; i >= 1; --i) v0[i] = std::min(v0[i], v0[i + 1] - 1);   // every group non-empty
+    for (int i = 1; i < G; ++i) v0[i] = std::max(v0[i], v0[i - 1] + 1);
+  }
   // requests sorted by vector, grouped
   std::vector<int> perm(n_req);
   for (int i = 0; i < n_req; ++i) perm[i] = i;

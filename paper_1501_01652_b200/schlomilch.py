@@ -187,7 +187,10 @@ class _Grid:
         del keep
         return F
 
-    HOST_GROUP_VECS = 8          # vectors per copy/compute group of apply_host
+    # apply_host vector groups: three tapered groups (sizes 1:4:1) measured
+    # best for cfg2 (64 vectors: 755 transforms/s e2e against 704 with two
+    # and 739 with five); each group boundary drains the far-field pipeline
+    HOST_GROUPS = 3
 
     def apply_host(self, requests, C, F, flags=_lib.FHTB_FAR | _lib.FHTB_NEAR, n_groups=None):
         """F = application of the requests, C and F pinned host float64
@@ -195,7 +198,7 @@ class _Grid:
         overlapped with the far field in vector groups.  Same bits as
         apply() on device copies with F = 0."""
         if n_groups is None:
-            n_groups = max(1, -(-C.shape[0] // self.HOST_GROUP_VECS))
+            n_groups = self.HOST_GROUPS if C.shape[0] >= 4 * self.HOST_GROUPS else 1
         arr, keep = _pack_requests(requests)
         ws_n = self._lib.fhtb_apply_host_workspace(self.handle, len(requests), C.shape[0], flags)
         ws = _device.workspace(ws_n)
