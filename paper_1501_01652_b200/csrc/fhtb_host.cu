@@ -37,8 +37,8 @@ int g_far_streams = 2;                     // far-field chunks in flight (direct
 int g_near_overlap = 1;                    // near field on its own stream beside the far field
 int g_prune_rows = 11;                     // narrow-row blocks: rows below 2^g_prune_rows
 int g_rowdot_bins = 1;                     // narrow-row blocks: at most this many pass-2 bins per column
-int g_min_lc = 9;
-int g_host_taper = 4;                      // fhtb_apply_host: inner/outer group size ratio                          // narrow-column blocks: smallest column FFT 2^g_min_lc
+int g_min_lc = 9;                          // narrow-column blocks: smallest column FFT 2^g_min_lc
+int g_host_taper = 4;                      // fhtb_apply_host: inner/outer group size ratio
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
