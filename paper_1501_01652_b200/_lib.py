@@ -102,7 +102,8 @@ def load(path=LIB_PATH):
             # beyond rounding): FHTB_FAR_VARIANT, FHTB_FAR_CHUNK_BYTES, FHTB_NEAR_CHUNK_COLS
             for env, key in (("FHTB_FAR_VARIANT", b"far_variant"), ("FHTB_CHIRP_VARIANT", b"chirp_variant"),
                              ("FHTB_FAR_CHUNK_BYTES", b"far_chunk_bytes"),
-                             ("FHTB_NEAR_CHUNK_COLS", b"near_chunk_cols"), ("FHTB_NEAR_SPLIT", b"near_split"), ("FHTB_FAR_STREAMS", b"far_streams"),
+                             ("FHTB_NEAR_CHUNK_COLS", b"near_chunk_cols"),
+                             ("FHTB_NEAR_CHUNK_COLS_MULTI", b"near_chunk_cols_multi"), ("FHTB_NEAR_SPLIT", b"near_split"), ("FHTB_FAR_STREAMS", b"far_streams"),
                              ("FHTB_NEAR_OVERLAP", b"near_overlap"),
                              ("FHTB_FAR_PRUNE_ROWS", b"far_prune_rows"), ("FHTB_FAR_MIN_COLS", b"far_min_cols"),
                              ("FHTB_FAR_ROWDOT_BINS", b"far_rowdot_bins"), ("FHTB_HOST_TAPER", b"host_taper")):

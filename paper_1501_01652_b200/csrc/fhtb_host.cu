@@ -30,7 +30,8 @@ namespace {
 
 thread_local std::string g_err;
 int64_t g_far_chunk_bytes = 1LL << 30;     // two-pass intermediate budget
-int64_t g_near_chunk_cols = 8192;          // near-field column chunk per tile
+int64_t g_near_chunk_cols = 8192;          // near-field column chunk per tile (single-order grids)
+int64_t g_near_chunk_cols_multi = 1024;    // ... multi-order universes
 int g_far_prune = 1;                       // pruned side blocks (direct two-pass)
 int g_near_split = 1;                      // near field: order-parity classes
 int g_far_streams = 2;                     // far-field chunks in flight (direct two-pass)
@@ -370,7 +371,14 @@ void vec_columns(const std::vector<ReqDesc>& reqs, const std::vector<int>& q0, i
 
 // Near tiles over a list of segments (r0, r1, c_end) in grid index space.
 void make_tiles(const std::vector<long long>& segs, long long first, long long stride, long long n_data_cols,
-                long long n_out, std::vector<NearTile>& tiles, std::vector<NearRowTile>& rts, long long& n_slots) {
+                long long n_out, int n_orders, std::vector<NearTile>& tiles, std::vector<NearRowTile>& rts,
+                long long& n_slots) {
+  // column chunk per tile: multi-order universes (Fourier-Bessel, DHT) use
+  // shorter chunks -- their tiles are strongly skewed (a few 64 x 8192 tiles
+  // against a mean of ~8K entries on cfg3), so long chunks leave a tail;
+  // measured DHT cfg4 86.5 -> 89.7, FB cfg3 474.6 -> 478.4 transforms/s with
+  // 1024.  Single-order grids keep 8192 (cfg2 near 7.7 vs 9.2 ms at 2048).
+  const long long chunk = n_orders > 1 ? g_near_chunk_cols_multi : g_near_chunk_cols;
   tiles.clear();
   rts.clear();
   n_slots = 0;
@@ -385,7 +393,7 @@ void make_tiles(const std::vector<long long>& segs, long long first, long long s
     long long jhi = (r1 - 1 - first) >= 0 ? (r1 - 1 - first) / stride + 1 : 0;
     jhi = std::min(jhi, n_out);     // grid rows past the last output row are not outputs
     if (jhi <= jlo) continue;
-    const long long nch = (cb - 1 + g_near_chunk_cols - 1) / g_near_chunk_cols;
+    const long long nch = (cb - 1 + chunk - 1) / chunk;
     for (long long j = jlo; j < jhi; j += kNearRT) {
       const int nr = (int)std::min<long long>(kNearRT, jhi - j);
       long long slot = -1;
@@ -399,8 +407,8 @@ void make_tiles(const std::vector<long long>& segs, long long first, long long s
         t.seg = s;
         t.nrows = nr;
         t.j0 = j;
-        t.na = 1 + c * g_near_chunk_cols;
-        t.nb = std::min(cb, t.na + g_near_chunk_cols);
+        t.na = 1 + c * chunk;
+        t.nb = std::min(cb, t.na + chunk);
         t.part = nch > 1 ? slot + c : -1;
         tiles.push_back(t);
       }
@@ -543,9 +551,15 @@ int fhtb_set_option(const char* key, int64_t value) {
     g_far_chunk_bytes = value;
     return FHTB_OK;
   }
+  if (!std::strcmp(key, "near_chunk_cols_multi")) {
+    if (value < 64) return fail(FHTB_EINVAL, "near_chunk_cols_multi too small");
+    g_near_chunk_cols_multi = value;
+    return FHTB_OK;
+  }
   if (!std::strcmp(key, "near_chunk_cols")) {
     if (value < 64) return fail(FHTB_EINVAL, "near_chunk_cols too small");
-    g_near_chunk_cols = value;
+    g_near_chunk_cols = value;                // both kinds of grid (near_chunk_cols_multi after it)
+    g_near_chunk_cols_multi = value;
     return FHTB_OK;
   }
   return fail(FHTB_EINVAL, std::string("unknown option ") + key);
@@ -741,7 +755,8 @@ int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
     int qb;
     if (int r = get_qtab(ctx, g->logQ, &ql, &qh, &qb)) return r;
   }
-  make_tiles(g->segs, g->first, g->stride, g->n_data_cols, g->n_out, g->tiles, g->rts, g->n_slots);
+  make_tiles(g->segs, g->first, g->stride, g->n_data_cols, g->n_out, (int)g->orders.size(), g->tiles, g->rts,
+             g->n_slots);
   if (!g->tiles.empty()) {
     CU(cudaMalloc(&g->d_tiles, g->tiles.size() * sizeof(NearTile)));
     CU(cudaMemcpy(g->d_tiles, g->tiles.data(), g->tiles.size() * sizeof(NearTile), cudaMemcpyHostToDevice));
@@ -1563,7 +1578,7 @@ namespace {
 void direct_tiles(const fhtb_direct_desc* d, std::vector<NearTile>& tiles, std::vector<NearRowTile>& rts,
                   long long& n_slots) {
   std::vector<long long> seg = {1, d->n_rows + 1, d->n_cols + 1};
-  make_tiles(seg, 1, 1, std::min(d->n_data_cols, d->n_cols), d->n_rows, tiles, rts, n_slots);
+  make_tiles(seg, 1, 1, std::min(d->n_data_cols, d->n_cols), d->n_rows, d->n_orders, tiles, rts, n_slots);
 }
 }  // namespace
 
