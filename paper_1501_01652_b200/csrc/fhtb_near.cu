@@ -58,7 +58,7 @@ __device__ __forceinline__ double ipow(double x, int p) {
 }
 
 template <int NORD, int JT>
-__global__ void __launch_bounds__(kNearThreads, 2)
+__global__ void __launch_bounds__(kNearThreads, (NORD == 1 && JT == 64) ? 3 : 2)
 near_kernel(NearArgs a) {
   using Cfg = NearCfg<NORD, JT>;
   constexpr int NK = Cfg::NK, K = Cfg::K, KA = Cfg::KA, JB = Cfg::JB;
