@@ -27,6 +27,7 @@
 //   reduce:  F[vec][j] += sum of the unit partials of that vector, in unit
 //            order (deterministic).
 #include <cuda.h>
+#include <algorithm>
 #include <cstring>
 
 #include "fhtb_core.cuh"
@@ -991,6 +992,25 @@ cudaError_t launch_far_colgen(const FarArgs& a, int logN1, int n_units, cudaStre
     case 12: return p2_d<4096, 2>(a, gx, n_units, st);
   }
   return cudaErrorInvalidValue;
+}
+
+// L2 prefetch of the coefficient rows of a chunk's units, launched just
+// before pass 1: the pass-1 prologue loads c strided by L1 columns at CTA
+// start, where its DRAM latency is exposed (~16% of pass-1 stall samples).
+__global__ void prefetch_rows_kernel(FarArgs a) {
+  const UnitDesc U = a.units[a.u0 + blockIdx.y];
+  const ReqDesc& R = a.reqs[U.req];
+  const double* row = a.C + (long long)R.vec * a.ldc;
+  const long long lines = (a.n_data_cols * 8 + 127) / 128;
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < lines; l += (long long)gridDim.x * blockDim.x)
+    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(row + l * 16));
+}
+
+cudaError_t launch_prefetch_rows(const FarArgs& a, int n_units, cudaStream_t st) {
+  const long long lines = (a.n_data_cols * 8 + 127) / 128;
+  const int bx = (int)std::min<long long>((lines + 255) / 256, 64);
+  note_launch(), prefetch_rows_kernel<<<dim3(bx, n_units), 256, 0, st>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_far_rowdot(const FarArgs& a, int n_units, int kbins, cudaStream_t st) {

@@ -39,6 +39,7 @@ int g_near_overlap = 1;                    // near field on its own stream besid
 int g_prune_rows = 11;                     // narrow-row blocks: rows below 2^g_prune_rows
 int g_rowdot_bins = 1;                     // narrow-row blocks: at most this many pass-2 bins per column
 int g_min_lc = 9;                          // narrow-column blocks: smallest column FFT 2^g_min_lc
+int g_far_prefetch = 1;                    // L2 prefetch of the coefficient rows before pass 1
 int g_host_taper = 4;                      // fhtb_apply_host: inner/outer group size ratio
 
 int fail(int code, const std::string& msg) {
@@ -503,6 +504,10 @@ int fhtb_set_option(const char* key, int64_t value) {
   if (!key) return fail(FHTB_EINVAL, "null key");
   if (!std::strcmp(key, "far_prune")) {
     g_far_prune = (int)value;
+    return FHTB_OK;
+  }
+  if (!std::strcmp(key, "far_prefetch")) {
+    g_far_prefetch = value ? 1 : 0;
     return FHTB_OK;
   }
   if (!std::strcmp(key, "host_taper")) {
@@ -1528,6 +1533,7 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
               a.part = b ? part2 : part;
               if (ci >= 2) CU(cudaStreamWaitEvent(cs, ax->red[b], 0));
             }
+            if (mode != 1 && g_far_prefetch) CU(launch_prefetch_rows(a, n_units, cs));
             if (mode == 1) {
               CU(launch_far_colgen(a, l1, n_units, cs));
             } else if (mode == 2) {
