@@ -107,7 +107,7 @@ def load(path=LIB_PATH):
                              ("FHTB_NEAR_OVERLAP", b"near_overlap"),
                              ("FHTB_FAR_PRUNE_ROWS", b"far_prune_rows"), ("FHTB_FAR_MIN_COLS", b"far_min_cols"),
                              ("FHTB_FAR_ROWDOT_BINS", b"far_rowdot_bins"), ("FHTB_HOST_TAPER", b"host_taper"),
-                             ("FHTB_FAR_PREFETCH", b"far_prefetch")):
+                             ("FHTB_FAR_PREFETCH", b"far_prefetch"), ("FHTB_NEAR_PRIORITY", b"near_priority")):
                 if os.environ.get(env):
                     lib.fhtb_set_option(key, int(os.environ[env]))
             _lib = lib

@@ -39,6 +39,7 @@ int g_near_overlap = 1;                    // near field on its own stream besid
 int g_prune_rows = 11;                     // narrow-row blocks: rows below 2^g_prune_rows
 int g_rowdot_bins = 1;                     // narrow-row blocks: at most this many pass-2 bins per column
 int g_min_lc = 9;                          // narrow-column blocks: smallest column FFT 2^g_min_lc
+int g_near_priority = 0;                   // near-field stream priority (see get_aux)
 int g_far_prefetch = 1;                    // L2 prefetch of the coefficient rows before pass 1
 int g_host_taper = 4;                      // fhtb_apply_host: inner/outer group size ratio
 
@@ -143,7 +144,12 @@ int get_aux(cudaStream_t caller, AuxStreams** out) {
       CU(cudaEventCreateWithFlags(&a.done[i], cudaEventDisableTiming));
       CU(cudaEventCreateWithFlags(&a.red[i], cudaEventDisableTiming));
     }
-    for (int i = 0; i < 3; ++i) CU(cudaStreamCreateWithFlags(&a.cs[i], cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) CU(cudaStreamCreateWithFlags(&a.cs[i], cudaStreamNonBlocking));
+    // near-field stream priority (near_priority: 0 = default, 1 = highest, -1 = lowest)
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    const int prio = g_near_priority > 0 ? hi : (g_near_priority < 0 ? lo : 0);
+    CU(cudaStreamCreateWithPriority(&a.cs[2], cudaStreamNonBlocking, prio));
     CU(cudaEventCreateWithFlags(&a.start, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&a.nstart, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&a.ndone, cudaEventDisableTiming));
@@ -504,6 +510,10 @@ int fhtb_set_option(const char* key, int64_t value) {
   if (!key) return fail(FHTB_EINVAL, "null key");
   if (!std::strcmp(key, "far_prune")) {
     g_far_prune = (int)value;
+    return FHTB_OK;
+  }
+  if (!std::strcmp(key, "near_priority")) {
+    g_near_priority = value > 0 ? 1 : (value < 0 ? -1 : 0);
     return FHTB_OK;
   }
   if (!std::strcmp(key, "far_prefetch")) {
