@@ -27,9 +27,13 @@ namespace fhtb {
 
 int g_chirp_variant = 0;   // tuning bits (performance only): 1 = pass 3 unbounded regs
 
+// x^p by binary powering (pre/post multipliers reach p = 10 per element)
 __device__ __forceinline__ double ipow_c(double x, int p) {
   double r = 1.0;
-  for (int i = 0; i < p; ++i) r *= x;
+  for (; p; p >>= 1) {
+    if (p & 1) r *= x;
+    x *= x;
+  }
   return r;
 }
 

@@ -35,9 +35,13 @@
 
 namespace fhtb {
 
+// x^p by binary powering (pre/post multipliers reach p = 10 per element)
 __device__ __forceinline__ double ipow_f(double x, int p) {
   double r = 1.0;
-  for (int i = 0; i < p; ++i) r *= x;
+  for (; p; p >>= 1) {
+    if (p & 1) r *= x;
+    x *= x;
+  }
   return r;
 }
 
