@@ -55,7 +55,9 @@ int fhtb_hankel_asy_eval(int nu, int m_terms, const double* z, int64_t n, double
 int fhtb_taylor_eval(int nu, int n_terms, const double* z, int64_t n, double* out, void* stream);
 /* First `count` roots of J0 and b_n = j_{0,n} - (n-1/4)pi; replaces
  * bessel.py:295-321.  Synchronous: *resid_max (host) = max |J0(root)|;
- * returns FHTB_ECONVERGE when it exceeds 1e-13 (bessel.py:313-317). */
+ * returns FHTB_ECONVERGE when a root's residual exceeds 1e-13
+ * (bessel.py:313-317) -- or, for roots beyond ~2e6 where the rounding of
+ * the root itself leaves |J0| above 1e-13, 2 ulp(root) |J1(root)|. */
 int fhtb_roots_j0(int64_t count, double* roots, double* perturb, double* resid_max, void* stream);
 /* Batched complex FFT (interleaved re/im), n = 2^k <= 2048, X_k = sum x_n e^{sign 2 pi i nk/n}.
  * Utility behind the FFT-core tests. */

@@ -929,6 +929,9 @@ static cudaError_t p1_d(const FarArgs& a, int n_units, cudaStream_t st) {
   if (N2 == 512) return p1_t<N2, E, 4, 3>(a, n_units, st);
   // 4096-point columns (narrow-row blocks): twiddles computed per use, 2 CTAs/SM
   if (N2 == 4096) return p1_t<N2, E, 1, 2, false>(a, n_units, st);
+  // 8192-point columns (grids 2L = 2^24, 2^25): twiddles per use, one CTA
+  // of 512 threads (the staged table would not fit beside the FFT buffer)
+  if (N2 == 8192) return p1_t<N2, E, 1, 1, false>(a, n_units, st);
   constexpr int W = N2 >= 4096 ? 1 : 4096 / N2;
   return p1_t<N2, E, W, 1>(a, n_units, st);
 }

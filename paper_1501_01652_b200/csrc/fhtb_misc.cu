@@ -91,6 +91,12 @@ __global__ void roots_j0_kernel(const JOrder* __restrict__ tab, long long count,
     pert[i] = x - g;
     const double r = fabs(jn(0, x, tab[0]));
     atomicMax(resid_bits, (unsigned long long)__double_as_longlong(r));
+    // residual against the tolerance this root can meet in fp64: the
+    // reference's 1e-13 (bessel.py:313), or, once the root's own rounding
+    // dominates (|J0(x)| ~ |J1(x)| ulp(x) reaches 1e-13 near x ~ 2e6, i.e.
+    // N ~ 2^20 roots), two ulps of x times |J1(x)|
+    const double tol = fmax(1e-13, 2.0 * fabs(jn(1, x, tab[1])) * (fabs(x) * 2.220446049250313e-16));
+    atomicMax(resid_bits + 1, (unsigned long long)__double_as_longlong(r / tol));
   }
 }
 

@@ -123,3 +123,37 @@ def test_host_buffer_path_bitwise(cuda_dev, n, nu, gamma, eps, batch):
             Fh = torch.full(C.shape, np.nan, dtype=torch.float64).pin_memory()
             g.apply_host(reqs, pinned, Fh, flags, n_groups=groups)
             assert torch.equal(Fh, Fd.cpu()), (flags, groups)
+
+
+@pytest.mark.parametrize("lg", [23, 24])
+def test_schlomilch_largest_grids_vs_direct_rows(cuda_dev, lg):
+    """BASELINE configs[4] reaches N = 2^24 (2L = 2^25: 8192-point pass-1
+    columns, narrow-row blocks capped at 8192-point columns)."""
+    n, eps = 2 ** lg, 1e-15
+    rng = np.random.default_rng([lg, 3])
+    C = torch.from_numpy(rng.standard_normal((1, n))).to(cuda_dev)
+    p = fh.select_params(0, n, eps)
+    F = fh.schlomilch_fast(p, C)
+    rows = _sample_rows(n, 120, lg)
+    k = torch.from_numpy(rows).to(cuda_dev)
+    col = (torch.arange(1, n + 1, dtype=torch.float64, device=cuda_dev) * np.pi).contiguous()
+    ref = _direct_rows((k.double() / n).contiguous(), col, 0, C)
+    err = float((F[0, k - 1] - ref[0]).abs().max())
+    assert err <= 10 * eps * float(C.abs().sum()), err
+
+
+def test_roots_beyond_two_million():
+    """2^20 + 1 roots (DHT N = 2^20): the largest roots sit where fp64
+    rounding of the root leaves |J0| above the reference's 1e-13; each root
+    is still within 2 ulp of its exact value (|J0| <= 2 ulp(x) |J1(x)|)."""
+    n = 2 ** 20 + 1
+    t = fh.bessel_roots_j0(n)
+    r = t.roots
+    assert r.shape == (n,) and np.all(np.diff(r) > 0)
+    assert abs(r[0] - 2.404825557695773) <= 1e-15
+    j0 = fh.bessel_j(0, r[-4096:])
+    j1 = fh.bessel_j(1, r[-4096:])
+    assert np.all(np.abs(j0) <= np.maximum(1e-13, 2 * np.abs(j1) * np.abs(r[-4096:]) * 2.0 ** -52))
+    # perturbation b_n = j_{0,n} - (n - 1/4) pi -> 1/(8 (n-1/4) pi) (McMahon)
+    nn = float(n)
+    assert abs(t.perturbations[-1] - 1.0 / (8 * (nn - 0.25) * np.pi)) <= 1e-9
