@@ -59,7 +59,9 @@ __device__ __forceinline__ double2 qtw_s(const FarArgs& a, long long m, int sign
 // the first radix pass is the half-zero DFT.  The four-step twiddles
 // e^{-2 pi i n1 k2/Q} of the thread's outputs are the same for every term:
 // built once into shared memory (thread-private slot-major slots).
-template <int N2, int E, int W, int MINB, bool HZ>
+// QT = false (8192-point columns): the four-step twiddles are formed per
+// use, the table would not fit beside the FFT buffer.
+template <int N2, int E, int W, int MINB, bool HZ, bool QT = true>
 __global__ void __launch_bounds__(W * (N2 / E), MINB)
 chirp_pass1_kernel(FarArgs a) {
   constexpr int T = N2 / E;
@@ -100,7 +102,8 @@ chirp_pass1_kernel(FarArgs a) {
   double2* sm = sm2 + w * NP;
   double2* qt = sm2 + W * NP + tid;
 #pragma unroll
-  for (int q = 0; q < E; ++q) qt[q * NTH] = qtw_s(a, n1 * fft_out_index<N2, E>(tt, q), -1);
+  for (int q = 0; q < E; ++q)
+    if (QT) qt[q * NTH] = qtw_s(a, n1 * fft_out_index<N2, E>(tt, q), -1);
   const double2* tw = a.tw + (N2 - 2);
   const int nterm = 2 * a.M;
   const int t0 = 2 * a.p0, t1 = 2 * a.p1;     // this shard's terms
@@ -127,7 +130,7 @@ chirp_pass1_kernel(FarArgs a) {
 #pragma unroll
     for (int q = 0; q < E; ++q) {
       const int k2 = fft_out_index<N2, E>(tt, q);
-      G[(long long)k2 * Q1 + n1] = cmul(z[q], qt[q * NTH]);
+      G[(long long)k2 * Q1 + n1] = cmul(z[q], QT ? qt[q * NTH] : qtw_s(a, n1 * k2, -1));
     }
   }
 }
@@ -410,11 +413,14 @@ static int pick_w(int N2) {
 
 template <int N2, int W>
 static cudaError_t c1_w(const FarArgs& a, int n_units, int hz, cudaStream_t st) {
-  constexpr int E = N2 >= 8 ? 8 : N2;
+  // 8192-point columns (Q = 2^25, the DHT at N = 2^24): 16 points per
+  // thread, one CTA per SM, twiddles per use
+  constexpr bool BIG = N2 >= 8192;
+  constexpr int E = BIG ? 16 : (N2 >= 8 ? 8 : N2);
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
-  const int smem = (W * (N2 + PAD) + W * N2) * 16;   // FFT buffers + four-step twiddles
-  constexpr int MB = (W * (N2 / E)) >= 256 ? 2 : 1;
-  auto k = (hz && E >= 8) ? chirp_pass1_kernel<N2, E, W, MB, true> : chirp_pass1_kernel<N2, E, W, MB, false>;
+  const int smem = (W * (N2 + PAD) + (BIG ? 0 : W * N2)) * 16;   // FFT buffers + four-step twiddles
+  constexpr int MB = BIG ? 1 : ((W * (N2 / E)) >= 256 ? 2 : 1);
+  auto k = (hz && E >= 8) ? chirp_pass1_kernel<N2, E, W, MB, true, !BIG> : chirp_pass1_kernel<N2, E, W, MB, false, !BIG>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   note_launch(), k<<<dim3(a.L1 / W, n_units), W * (N2 / E), smem, st>>>(a);
@@ -423,10 +429,11 @@ static cudaError_t c1_w(const FarArgs& a, int n_units, int hz, cudaStream_t st) 
 
 template <int N2, int W>
 static cudaError_t c3_w(const FarArgs& a, int n_ranges, cudaStream_t st) {
-  constexpr int E = N2 >= 8 ? 8 : N2;
+  constexpr bool BIG = N2 >= 8192;          // see c1_w
+  constexpr int E = BIG ? 16 : (N2 >= 8 ? 8 : N2);
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
   const int smem = W * (N2 + PAD) * 16;
-  constexpr int MB = (W * (N2 / E)) >= 256 ? 2 : 1;
+  constexpr int MB = BIG ? 1 : ((W * (N2 / E)) >= 256 ? 2 : 1);
   auto k = (g_chirp_variant & 1) ? chirp_pass3_kernel<N2, E, W, 1> : chirp_pass3_kernel<N2, E, W, MB>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;

@@ -465,7 +465,8 @@ struct fhtb_grid {
 namespace {
 
 void split_q(int logQ, int* l1, int* l2) {
-  *l1 = (logQ + 1) / 2;
+  // pass 2 holds three N1-point rows in shared memory: N1 <= 4096
+  *l1 = std::min(12, (logQ + 1) / 2);
   *l2 = logQ - *l1;
 }
 

@@ -157,3 +157,22 @@ def test_roots_beyond_two_million():
     # perturbation b_n = j_{0,n} - (n - 1/4) pi -> 1/(8 (n-1/4) pi) (McMahon)
     nn = float(n)
     assert abs(t.perturbations[-1] - 1.0 / (8 * (nn - 0.25) * np.pi)) <= 1e-9
+
+
+@pytest.mark.parametrize("lg,eps", [(22, 1e-8), (24, 1e-3)])
+def test_dht_largest_grids_vs_direct_rows(cuda_dev, lg, eps):
+    """BASELINE configs[4] DHT up to N = 2^24 (chirp length 2^25: 8192-point
+    chirp columns, 4096-point rows): sampled rows against direct fp64 sums
+    sum_n c_n J0(j_k j_n / j_{N+1})."""
+    n = 2 ** lg
+    plan = fh.dht_plan(n, eps)
+    C = torch.from_numpy(np.random.default_rng([lg, 5]).standard_normal((1, n))).to(cuda_dev)
+    F = fh.dht(plan, C)
+    r_dev, _ = plan.roots.device_arrays()
+    rows = _sample_rows(n, 80, lg)
+    k = torch.from_numpy(rows).to(cuda_dev)
+    scale = (r_dev[k - 1] / r_dev[n]).contiguous()
+    ref = torch.zeros((1, rows.size), dtype=torch.float64, device=cuda_dev)
+    _direct_apply(scale, r_dev, n, [0], [dict(vec=0, terms=[(0, 1.0)])], C, ref)
+    err = float((F[0, k - 1] - ref[0]).abs().max())
+    assert err <= 10 * eps * float(C.abs().sum()), err
