@@ -175,3 +175,18 @@ def test_alltoall_falls_back_without_full_blocks(cuda_dev):
     outs, rounds = _exchange_split(fn, 3)
     assert rounds == {0: 0, 1: 0, 2: 0}
     assert _close(outs[0] + outs[1] + outs[2], full, C.cpu().numpy())
+
+
+def test_alltoall_single_2_24_transform_over_8(cuda_dev):
+    """BASELINE configs[4]: one N = 2^24 transform split over 8 ranks with the
+    all-to-all four-step (2L = 2^25: 8192-point pass-1 column slabs of 512
+    columns per rank); the rank outputs sum to the one-GPU transform."""
+    n, eps = 2 ** 24, 1e-15
+    C = torch.from_numpy(np.random.default_rng(24).standard_normal((1, n))).to(cuda_dev)
+    params = fh.select_params(0, n, eps)
+    fn = lambda: fh.schlomilch_fast(params, C)
+    full = fn()
+    outs, rounds = _exchange_split(fn, 8)
+    assert all(v == rounds[0] and v >= 1 for v in rounds.values())
+    tot = torch.stack(outs).sum(0)
+    assert float((tot - full).abs().max()) <= 2e-15 * float(C.abs().sum())
