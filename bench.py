@@ -339,37 +339,38 @@ def run_tasks(fh, dev, rank, world, steps, warmup):
 
     from paper_1501_01652_b200.fourier_bessel import select_neumann_params
     from paper_1501_01652_b200.schlomilch import SchlomilchEngine, _m_terms
-    # FB cfg3
-    n, B, eps = 2 ** 18, 16, 1e-12
-    roots = fh.bessel_roots_j0(n)
-    C = torch.from_numpy(np.stack([rng("u", n, b) for b in range(B)])).to(dev)
-    ms = timed(lambda: fh.fourier_bessel_eval(0, C, eps, roots=roots))
-    q = select_neumann_params(eps)
-    R = 2 * q.t_terms + q.k_terms - 2
-    eng = SchlomilchEngine(n, -0.25, eps / R, range(q.k_terms))
-    bpv = R * model_bytes(eng.params, eng.scheme)
-    out["fb_cfg3"] = {"config": "Fourier-Bessel order 0, N=2^18, 16 vectors U[-1,1], eps=1e-12",
-                      "transforms_per_s": B * world / (ms / 1e3), "ms_per_step": ms,
-                      "model_bytes_per_vector": bpv,
-                      "model_frac_of_hbm": bpv * B / (ms / 1e3) / 1e9 / peak}
-    # DHT cfg4
-    n, B, eps = 2 ** 16, 8, 1e-15
-    plan = fh.dht_plan(n, eps)
-    C = torch.from_numpy(np.stack([rng("n", n, b) for b in range(B)])).to(dev)
-    st_ = {}
-    fh.dht(plan, C[:1], stats=st_)
-    ms = timed(lambda: fh.dht(plan, C))
-    from paper_1501_01652_b200.dht import _shared
-    eng = _shared(plan)["engine"]
-    reqs = st_.get("schlomilch_evaluations", 0)
-    T = 2 * eng.params.m_terms * len(eng.scheme.blocks)
-    L2 = 1 << int(math.ceil(math.log2(2 * n - 1)))
-    bpv = reqs * (T * 2 * 32 * L2 + len(eng.scheme.blocks) * 8 * n + 8 * n)
-    out["dht_cfg4"] = {"config": "DHT order 0, N=2^16, 8 vectors N(0,1), eps=1e-15",
-                       "transforms_per_s": B * world / (ms / 1e3), "ms_per_step": ms,
-                       "requests_per_vector": reqs, "model": "row-restricted chirp-z (SURVEY 8(d))",
-                       "model_bytes_per_vector": bpv,
-                       "model_frac_of_hbm": bpv * B / (ms / 1e3) / 1e9 / peak}
+    def fb_task(n, B, eps, key, desc):
+        roots = fh.bessel_roots_j0(n)
+        C = torch.from_numpy(np.stack([rng("u", n, b) for b in range(B)])).to(dev)
+        ms = timed(lambda: fh.fourier_bessel_eval(0, C, eps, roots=roots))
+        q = select_neumann_params(eps)
+        R = 2 * q.t_terms + q.k_terms - 2
+        eng = SchlomilchEngine(n, -0.25, eps / R, range(q.k_terms))
+        bpv = R * model_bytes(eng.params, eng.scheme)
+        out[key] = {"config": desc, "transforms_per_s": B * world / (ms / 1e3), "ms_per_step": ms,
+                    "model_bytes_per_vector": bpv, "model_frac_of_hbm": bpv * B / (ms / 1e3) / 1e9 / peak}
+
+    def dht_task(n, B, eps, key, desc):
+        plan = fh.dht_plan(n, eps)
+        C = torch.from_numpy(np.stack([rng("n", n, b) for b in range(B)])).to(dev)
+        st_ = {}
+        fh.dht(plan, C[:1], stats=st_)
+        ms = timed(lambda: fh.dht(plan, C))
+        from paper_1501_01652_b200.dht import _shared
+        eng = _shared(plan)["engine"]
+        reqs = st_.get("schlomilch_evaluations", 0)
+        T = 2 * eng.params.m_terms * len(eng.scheme.blocks)
+        L2 = 1 << int(math.ceil(math.log2(2 * n - 1)))
+        bpv = reqs * (T * 2 * 32 * L2 + len(eng.scheme.blocks) * 8 * n + 8 * n)
+        out[key] = {"config": desc, "transforms_per_s": B * world / (ms / 1e3), "ms_per_step": ms,
+                    "requests_per_vector": reqs, "model": "row-restricted chirp-z (SURVEY 8(d))",
+                    "model_bytes_per_vector": bpv, "model_frac_of_hbm": bpv * B / (ms / 1e3) / 1e9 / peak}
+
+    fb_task(2 ** 18, 16, 1e-12, "fb_cfg3", "Fourier-Bessel order 0, N=2^18, 16 vectors U[-1,1], eps=1e-12")
+    dht_task(2 ** 16, 8, 1e-15, "dht_cfg4", "DHT order 0, N=2^16, 8 vectors N(0,1), eps=1e-15")
+    # the metric's N = 2^20 for the other two tasks (BASELINE.json metric)
+    fb_task(2 ** 20, 16, 1e-12, "fb_n2^20", "Fourier-Bessel order 0, N=2^20, 16 vectors U[-1,1], eps=1e-12")
+    dht_task(2 ** 20, 4, 1e-15, "dht_n2^20", "DHT order 0, N=2^20, 4 vectors N(0,1), eps=1e-15")
     # cfg2 at the looser eps
     n, B = 2 ** 20, 64
     Cs = torch.from_numpy(make_inputs(n, B, rank)).to(dev)
