@@ -41,7 +41,7 @@ int g_rowdot_bins = 1;                     // narrow-row blocks: at most this ma
 int g_min_lc = 9;                          // narrow-column blocks: smallest column FFT 2^g_min_lc
 int g_near_priority = 0;                   // near-field stream priority (see get_aux)
 int g_far_prefetch = 1;                    // L2 prefetch of the coefficient rows before pass 1
-int g_host_taper = 4;                      // fhtb_apply_host: inner/outer group size ratio
+int g_host_taper = 8;                      // fhtb_apply_host: inner/outer group size ratio
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -1225,14 +1225,17 @@ int fhtb_apply_host(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req,
                                0, 1, nullptr, base + hl.far_off, hl.far_bytes, st))
           return r;
     }
-    if (near) {
-      CU(cudaStreamWaitEvent(st, hx->ndone, 0));
-      if (far) CU(launch_add_rows(Fg, ldf, Fn + (size_t)v0[i] * ldf, ldf, nv, ldf, st));
-    } else if (!far) {
-      CU(cudaMemsetAsync(Fg, 0, sizeof(double) * (size_t)nv * ldf, st));
-    }
+    if (!near && !far) CU(cudaMemsetAsync(Fg, 0, sizeof(double) * (size_t)nv * ldf, st));
+    // the near-field add and the copy-out of group i run on the d2h stream:
+    // the caller's stream goes straight on to the far field of group i+1
+    // instead of waiting there for the near field (which needs every group's
+    // rows and so finishes only after the first groups' far fields)
     CU(cudaEventRecord(hx->fin[i], st));
     CU(cudaStreamWaitEvent(hx->d2h, hx->fin[i], 0));
+    if (near) {
+      CU(cudaStreamWaitEvent(hx->d2h, hx->ndone, 0));
+      if (far) CU(launch_add_rows(Fg, ldf, Fn + (size_t)v0[i] * ldf, ldf, nv, ldf, hx->d2h));
+    }
     CU(cudaMemcpy2DAsync(F_host + (size_t)v0[i] * ldf_host, ldf_host * sizeof(double), Fg, ldf * sizeof(double),
                          ldf * sizeof(double), nv, cudaMemcpyDeviceToHost, hx->d2h));
   }

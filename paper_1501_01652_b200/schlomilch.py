@@ -187,10 +187,12 @@ class _Grid:
         del keep
         return F
 
-    # apply_host vector groups: three tapered groups (sizes 1:4:1) measured
-    # best for cfg2 (64 vectors: 755 transforms/s e2e against 704 with two
-    # and 739 with five); each group boundary drains the far-field pipeline
-    HOST_GROUPS = 3
+    # apply_host vector groups: up to eight tapered groups (end groups 1/8 of
+    # the inner ones), at least 8 vectors per group; measured on cfg2 (64
+    # vectors, e2e transforms/s): 2 groups 719, 3 773, 4 795, 8 798, 10 799,
+    # 16 788
+    HOST_GROUPS = 8
+    HOST_GROUP_MIN_VECS = 8
 
     def apply_host(self, requests, C, F, flags=_lib.FHTB_FAR | _lib.FHTB_NEAR, n_groups=None):
         """F = application of the requests, C and F pinned host float64
@@ -198,7 +200,7 @@ class _Grid:
         overlapped with the far field in vector groups.  Same bits as
         apply() on device copies with F = 0."""
         if n_groups is None:
-            n_groups = self.HOST_GROUPS if C.shape[0] >= 4 * self.HOST_GROUPS else 1
+            n_groups = min(self.HOST_GROUPS, max(1, C.shape[0] // self.HOST_GROUP_MIN_VECS))
         arr, keep = _pack_requests(requests)
         ws_n = self._lib.fhtb_apply_host_workspace(self.handle, len(requests), C.shape[0], flags)
         ws = _device.workspace(ws_n)
