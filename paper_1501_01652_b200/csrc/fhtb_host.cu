@@ -41,7 +41,7 @@ int g_rowdot_bins = 1;                     // narrow-row blocks: at most this ma
 int g_min_lc = 9;                          // narrow-column blocks: smallest column FFT 2^g_min_lc
 int g_near_priority = 0;                   // near-field stream priority (see get_aux)
 int g_far_prefetch = 1;                    // L2 prefetch of the coefficient rows before pass 1
-int g_host_taper = 8;                      // fhtb_apply_host: inner/outer group size ratio
+int g_host_taper = 4;                      // fhtb_apply_host: inner/outer group size ratio
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -1023,9 +1023,19 @@ size_t x_ws(const fhtb_grid* g, int n_req, int world, size_t xbytes) {
          align_up(sizeof(double) * u_round * (size_t)g->n_out) + 4096;
 }
 
+// fhtb_apply_host's far-field calls: the group's rows are ready when `ready`
+// fires, and its workspace region is free when `region_free` fires (null: no
+// earlier user).  The tables are then copied on the first auxiliary far
+// stream and only the aux streams wait, so the chunks of consecutive groups
+// follow each other on the aux streams without draining the pipeline.
+struct HostPipe {
+  cudaEvent_t ready;
+  cudaEvent_t region_free;
+};
+
 int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C, int64_t ldc,
                int32_t n_vec, double* F, int64_t ldf, int32_t flags, int32_t shard, int32_t n_shards,
-               const XCtx* xc, void* ws, size_t ws_bytes, void* stream);
+               const XCtx* xc, void* ws, size_t ws_bytes, void* stream, const HostPipe* hp = nullptr);
 
 }  // namespace
 
@@ -1127,9 +1137,9 @@ HostLayout host_layout(const fhtb_grid* g, int32_t n_req, int32_t n_vec, int32_t
   const bool near = (flags & FHTB_NEAR) && !g->tiles.empty();
   h.fn_off = s;
   if (near && (flags & FHTB_FAR)) s += align_up(sizeof(double) * (size_t)n_vec * g->n_out);
-  h.far_off = s;
+  h.far_off = s;                             // two far regions, alternating groups
   h.far_bytes = (flags & FHTB_FAR) ? ws_need(g, n_req, n_vec, FHTB_FAR) : 0;
-  s += align_up(h.far_bytes);
+  s += 2 * align_up(h.far_bytes);
   h.near_off = s;
   h.near_bytes = near ? ws_need(g, n_req, n_vec, FHTB_NEAR) : 0;
   s += align_up(h.near_bytes);
@@ -1218,11 +1228,13 @@ int fhtb_apply_host(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req,
         sub.push_back(r);
         ++q;
       }
-      CU(cudaStreamWaitEvent(st, hx->in[i], 0));
       CU(cudaMemsetAsync(Fg, 0, sizeof(double) * (size_t)nv * ldf, st));
+      // region i % 2 was last used by group i - 2 (done when fin[i-2] fired)
+      const HostPipe hp{hx->in[i], i >= 2 ? hx->fin[i - 2] : nullptr};
       if (!sub.empty())
         if (int r = apply_impl(g, sub.data(), (int)sub.size(), Cd + (size_t)v0[i] * ldc, ldc, nv, Fg, ldf, FHTB_FAR,
-                               0, 1, nullptr, base + hl.far_off, hl.far_bytes, st))
+                               0, 1, nullptr, base + hl.far_off + (i & 1) * align_up(hl.far_bytes), hl.far_bytes,
+                               st, &hp))
           return r;
     }
     if (!near && !far) CU(cudaMemsetAsync(Fg, 0, sizeof(double) * (size_t)nv * ldf, st));
@@ -1342,8 +1354,9 @@ int run_exchange(const fhtb_grid* g, DevCtx* ctx, const std::vector<ReqDesc>& rs
 
 int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C, int64_t ldc,
                int32_t n_vec, double* F, int64_t ldf, int32_t flags, int32_t shard, int32_t n_shards,
-               const XCtx* xc, void* ws, size_t ws_bytes, void* stream) {
+               const XCtx* xc, void* ws, size_t ws_bytes, void* stream, const HostPipe* hp) {
   if (!g) return fail(FHTB_EINVAL, "null grid");
+  if (hp && (flags != FHTB_FAR || xc || n_shards != 1)) return fail(FHTB_EINVAL, "host pipe: far field only");
   if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(FHTB_EINVAL, "bad shard index");
   if (n_req < 0 || n_vec < 0) return fail(FHTB_EINVAL, "negative counts");
   if (n_req == 0 || n_vec == 0) return FHTB_OK;
@@ -1365,7 +1378,7 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
 
   Carve cv{(char*)ws, ws_bytes};
   ReqDesc* d_req = cv.take<ReqDesc>(n_req);
-  CU(cudaMemcpyAsync(d_req, rs.data(), n_req * sizeof(ReqDesc), cudaMemcpyHostToDevice, st));
+  if (!hp) CU(cudaMemcpyAsync(d_req, rs.data(), n_req * sizeof(ReqDesc), cudaMemcpyHostToDevice, st));
 
   // Near field concurrently with the far field (both requested): it runs on
   // an auxiliary stream into a separate buffer Fn, added to F at the end on
@@ -1482,8 +1495,16 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
       if (pipe) {
         if (int r = get_aux(st, &ax)) return r;
       }
-      CU(cudaMemcpyAsync(d_units, fp.units.data(), nu * sizeof(UnitDesc), cudaMemcpyHostToDevice, st));
-      CU(cudaMemcpyAsync(d_ch, fp.chunks.data(), fp.chunks.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+      // tables: on the caller's stream, or (host pipe) on the first aux stream
+      cudaStream_t ts = st;
+      if (hp) {
+        ts = pipe ? ax->cs[0] : st;
+        CU(cudaStreamWaitEvent(ts, hp->ready, 0));
+        if (hp->region_free) CU(cudaStreamWaitEvent(ts, hp->region_free, 0));
+        CU(cudaMemcpyAsync(d_req, rs.data(), n_req * sizeof(ReqDesc), cudaMemcpyHostToDevice, ts));
+      }
+      CU(cudaMemcpyAsync(d_units, fp.units.data(), nu * sizeof(UnitDesc), cudaMemcpyHostToDevice, ts));
+      CU(cudaMemcpyAsync(d_ch, fp.chunks.data(), fp.chunks.size() * sizeof(int2), cudaMemcpyHostToDevice, ts));
       FarArgs a;
       std::memset(&a, 0, sizeof a);
       a.L = g->L;
@@ -1520,7 +1541,12 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
         CU(launch_far_onepass(a, g->logN1, (int)nu, st));
         CU(launch_far_reduce(a, (int)nu, st));
       } else {
-        if (pipe) {
+        if (pipe && hp) {
+          // the second aux stream and the reductions wait for the tables only
+          CU(cudaEventRecord(ax->start, ax->cs[0]));
+          CU(cudaStreamWaitEvent(ax->cs[1], ax->start, 0));
+          CU(cudaStreamWaitEvent(st, ax->start, 0));
+        } else if (pipe) {
           // the aux streams start after the caller's prior work (C, F ready)
           CU(cudaEventRecord(ax->start, st));
           for (int b = 0; b < 2; ++b) CU(cudaStreamWaitEvent(ax->cs[b], ax->start, 0));

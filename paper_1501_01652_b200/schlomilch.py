@@ -187,7 +187,7 @@ class _Grid:
         del keep
         return F
 
-    # apply_host vector groups: up to eight tapered groups (end groups 1/8 of
+    # apply_host vector groups: up to eight tapered groups (end groups 1/4 of
     # the inner ones), at least 8 vectors per group; measured on cfg2 (64
     # vectors, e2e transforms/s): 2 groups 719, 3 773, 4 795, 8 798, 10 799,
     # 16 788
