@@ -282,7 +282,9 @@ def run_ours(args):
                      "peak_source": peak_src,
                      "limiter_evidence": bounds_from_profile()},
         "e2e": {"value": batch * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(host.nbytes),
-                "d2h_bytes_per_step": int(out.nbytes)},
+                "d2h_bytes_per_step": int(out.nbytes),
+                "path": "schlomilch_fast(pinned CPU tensor) -> fhtb_apply_host: copies in/out overlapped with "
+                        "the far field in tapered vector groups; median of %d calls" % max(1, min(args.steps, 5))},
         "gpu_launches": int(l1 - l0),
         "clocks": clocks,
         "tasks": tasks,
