@@ -925,8 +925,26 @@ static cudaError_t p1_t(const FarArgs& a, int n_units, cudaStream_t st) {
 template <int N2>
 static cudaError_t p1_d(const FarArgs& a, int n_units, cudaStream_t st) {
   constexpr int E = N2 >= 16 ? 16 : N2;
-  // 512-point columns: 128-thread CTAs, 3 per SM (as the tuned 1024 shape)
-  if (N2 == 512) return p1_t<N2, E, 4, 3>(a, n_units, st);
+  // 512-point columns: 128-thread CTAs, 3 per SM (as the tuned 1024 shape);
+  // bits 24-27 of the variant select alternatives (tuning sweeps; measured
+  // on FB cfg3: default 487, W=8/2 CTAs 470, W=4/2 CTAs 483, W=2/4 CTAs 486)
+  if (N2 == 512) {
+    switch ((g_far_variant >> 24) & 15) {
+      case 1: return p1_t<N2, E, 8, 2>(a, n_units, st);
+      case 2: return p1_t<N2, E, 4, 2>(a, n_units, st);
+      case 3: return p1_t<N2, E, 2, 4>(a, n_units, st);
+      default: return p1_t<N2, E, 4, 3>(a, n_units, st);
+    }
+  }
+  // 2048-point columns: bits 28-30 (default: 2 columns per CTA, 1 CTA/SM;
+  // one column at 2 or 3 CTAs/SM measured 8-12% slower on FB cfg3 and cfg2 1e-8)
+  if (N2 == 2048) {
+    switch ((g_far_variant >> 28) & 7) {
+      case 1: return p1_t<N2, E, 1, 2>(a, n_units, st);
+      case 2: return p1_t<N2, E, 1, 3>(a, n_units, st);
+      default: break;
+    }
+  }
   // 4096-point columns (narrow-row blocks): twiddles computed per use, 2 CTAs/SM
   if (N2 == 4096) return p1_t<N2, E, 1, 2, false>(a, n_units, st);
   // 8192-point columns (grids 2L = 2^24, 2^25): twiddles per use, one CTA
