@@ -29,7 +29,7 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 namespace {
 
 thread_local std::string g_err;
-int64_t g_far_chunk_bytes = 1LL << 30;     // two-pass intermediate budget
+int64_t g_far_chunk_bytes = 2LL << 30;     // two-pass intermediate budget per chunk (2 GiB measured best: cfg2 step 77.65 -> 76.85 ms; 1.5 GiB 77.25, 3 GiB 79.3)
 int64_t g_near_chunk_cols = 8192;          // near-field column chunk per tile (single-order grids)
 int64_t g_near_chunk_cols_multi = 1024;    // ... multi-order universes
 int g_far_prune = 1;                       // pruned side blocks (direct two-pass)
