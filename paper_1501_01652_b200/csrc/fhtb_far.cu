@@ -252,6 +252,9 @@ far_pass1p_kernel(FarArgs a) {
 // r_0 and the MODE-2 column-shift phase phi_k are applied once at the end.
 // MODE 3: MODE 0 in exchange mode (distributed four-step): column pairs from
 //         a.xc0, rows assembled from the received chunks of all ranks.
+// step-table twiddles for narrow-column blocks: always at E = 16; at E = 8
+// only in the high-occupancy shapes (MINB >= 5), which need the registers
+#define TQS_ON(MODE, E, MINB) ((MODE) == 2 && ((E) >= 16 || (MINB) >= 5))
 #define TQS_SMEM(MODE, E) ((MODE) == 2 && (E) >= 16)
 #define IRS_K(E, MODE) false
 template <int N1, int E, int MODE, int MINB>
@@ -292,7 +295,7 @@ far_pass2_kernel(FarArgs a) {
   // ([q][tid] after the FFT buffers) instead of NQ registers, which the
   // 16-point state cannot spare without spilling
   constexpr bool IRS = false;   // (measured: 18.05 -> 18.30 ms at 2048 points, so off)
-  double* irs = reinterpret_cast<double*>(sm2 + NCOL * NP + (TQS_SMEM(MODE, E) ? NCOL * E : 0));
+  double* irs = reinterpret_cast<double*>(sm2 + NCOL * NP + (TQS_ON(MODE, E, MINB) ? NCOL * E : 0));
   int* kqs = reinterpret_cast<int*>(irs + (IRS ? NQ * NT : 0));      // IRS: row indices too
   double ir[IRS ? 1 : NQ], rp[HOR ? 1 : NQ];
   double2 acc[NQ];
@@ -333,7 +336,7 @@ far_pass2_kernel(FarArgs a) {
   //           thread and st[e] = e^{2 pi i T e k2/Q} per column in shared
   //           memory (broadcast reads): E complex registers fewer, which
   //           lets the column FFT run with E = 16 (one radix pass fewer)
-  constexpr bool TQS = (MODE == 2 && E >= 16);
+  constexpr bool TQS = TQS_ON(MODE, E, MINB);
   double v[ONEPASS ? E : 1], iw[ONEPASS ? E : 1];
   double2 tq[(MODE == 2 && !TQS) ? E : 1];
   double2 tb = make_double2(1.0, 0.0);
@@ -871,7 +874,7 @@ __global__ void far_reduce_kernel(FarArgs a, int n_units) {
 // bits 0-3: pass-1 shape at 1024; 4-7: pass-2 shape at 2048; 8-11: paired-lane
 // pass 2; 12-15: per-pair pass 1; bit 16: no TMA stores; 20-23: narrow-column
 // FFT shape.  Default = best measured on B200.
-int g_far_variant = 20 + (1 << 20);
+int g_far_variant = 20 + (3 << 20);
 
 // 2D tensor map over G viewed as rows of 2*L1 doubles (one row per (unit,
 // pair, k2)); cuTensorMapEncodeTiled is fetched through the runtime so the
@@ -958,7 +961,7 @@ template <int N1, int E, int MODE, int MINB>
 static cudaError_t p2_t(const FarArgs& a, int gx, int gy, cudaStream_t st) {
   constexpr int T = N1 / E;
   constexpr int NCOL = MODE == 1 ? 1 : 2;
-  const int smem = (NCOL * (N1 + 4) + (TQS_SMEM(MODE, E) ? NCOL * E : 0)) * 16 +
+  const int smem = (NCOL * (N1 + 4) + (TQS_ON(MODE, E, MINB) ? NCOL * E : 0)) * 16 +
                    (IRS_K(E, MODE) ? (E / 2) * NCOL * T * 12 : 0);   // + IRS row factors, rows
   auto k = far_pass2_kernel<N1, E, MODE, MINB>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -985,6 +988,14 @@ static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
       // 512 columns 14.6 -> 15.6 ms, so they keep E = 8 under case 1
       case 1: if (N1 >= 1024) return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : 3)>(a, gx, gy, st); break;
       case 2: return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : N1 >= 1024 ? 3 : 6)>(a, gx, gy, st);
+      // case 3 (default): 512 columns at 5 CTAs/SM with step-table twiddles
+      // (cfg2 far 70.8 -> 70.6 ms; 6 CTAs/SM 71.4)
+      case 3: if (N1 == 512) return p2_t<N1, 8, MODE, 5>(a, gx, gy, st);
+              if (N1 >= 1024) return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : 3)>(a, gx, gy, st);
+              break;
+      case 4: if (N1 == 512) return p2_t<N1, 8, MODE, 6>(a, gx, gy, st);
+              if (N1 >= 1024) return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : 3)>(a, gx, gy, st);
+              break;
       default: break;
     }
   }
