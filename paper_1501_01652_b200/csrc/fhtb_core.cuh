@@ -286,7 +286,11 @@ __device__ __forceinline__ void stockham_mid(double2 (&v)[E], double2* sm, int t
 // `sm` from a previous use (a __syncthreads before the call).
 // HZ: the upper half of the thread's first-pass inputs (slots e >= E/2) is
 // zero, except `extra` added to slot E/2 (a single element, 0 elsewhere).
-template <int N, int E, int S, bool HZ = false>
+// SYNC0: the caller has NOT synchronised; the CTA barrier (preceded, in
+// thread t == 0, by the wait for the reads of the previous TMA store from
+// `sm`) is taken after the register-only first pass, so that pass overlaps
+// the barrier wait and the bulk copy still reading shared memory.
+template <int N, int E, int S, bool HZ = false, bool SYNC0 = false>
 __device__ __forceinline__ void block_fft(double2 (&v)[E], double2* sm, int t,
                                           const double2* __restrict__ tw,
                                           double2 extra = make_double2(0.0, 0.0)) {
@@ -301,6 +305,10 @@ __device__ __forceinline__ void block_fft(double2 (&v)[E], double2* sm, int t,
     }
   } else {
     Dft<E, S>::run(v);
+  }
+  if (SYNC0) {
+    if (t == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncthreads();
   }
   if (Sh::NPASS == 1) return;
 #pragma unroll

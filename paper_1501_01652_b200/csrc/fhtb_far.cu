@@ -137,9 +137,14 @@ far_pass1_kernel(FarArgs a, const __grid_constant__ CUtensorMap gmap) {
     const double ims = vs * iws;
     const double2 extra = make_double2(vs, ims);
     vs = ims * iws;
-    if (TMA && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    __syncthreads();
-    block_fft<N2, E, 1, true>(z, sm, tt, tw, extra);
+    if (TMA) {
+      // the previous pair's tensor store may still read the staging area:
+      // waited for after the register-only first radix pass (SYNC0)
+      block_fft<N2, E, 1, true, true>(z, sm, tt, tw, extra);
+    } else {
+      __syncthreads();
+      block_fft<N2, E, 1, true>(z, sm, tt, tw, extra);
+    }
     if (TMA) {
       __syncthreads();
 #pragma unroll
