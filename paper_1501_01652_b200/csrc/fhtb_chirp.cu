@@ -402,6 +402,62 @@ trig_kernel(int kind, long long n, long long L, long long k0, long long n0, cons
   }
 }
 
+// Lengths with Q > 8192 (any length, trig.py:80-92 has no cap): the same
+// chirp-z convolution on the multi-pass power-of-two FFT (plain_fft), per row:
+//   A = v * in-chirp (zero padded to Q);  A2 = FFT(A);  A = conj(A2 * H);
+//   A2 = FFT(A)  (= conj of the unnormalised inverse FFT of A2 * H);
+//   out = Re/Im(conj(A2) * out-chirp) / Q.
+__global__ void trig_pre_kernel(const double* __restrict__ x, long long n, long long L, long long k0,
+                                long long Q, double2* __restrict__ A) {
+  for (long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x; m < Q; m += (long long)gridDim.x * blockDim.x) {
+    double2 z = make_double2(0.0, 0.0);
+    if (m < n) {
+      const double2 c = chirpE(2 * k0 * m + ((m * m) % (4 * L)), L);
+      const double xv = x[m];
+      z = make_double2(xv * c.x, xv * c.y);
+    }
+    A[m] = z;
+  }
+}
+
+__global__ void trig_mid_kernel(const double2* __restrict__ A2, const double2* __restrict__ H, long long Q,
+                                double2* __restrict__ A) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < Q; i += (long long)gridDim.x * blockDim.x)
+    A[i] = cconj(cmul(A2[i], __ldg(H + i)));
+}
+
+__global__ void trig_post_kernel(int kind, const double2* __restrict__ A2, long long n, long long L, long long k0,
+                                 long long n0, long long Q, double* __restrict__ o) {
+  const double inv = 1.0 / (double)Q;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const long long P = 2 * k0 * n0 + 2 * j * n0 + ((j * j) % (4 * L));
+    const double2 Y = cmul(cconj(A2[j]), chirpE(P, L));
+    o[j] = (kind == 0 ? Y.x : Y.y) * inv;
+  }
+}
+
+static unsigned ew_blocks(long long n) {
+  long long b = (n + 255) / 256;
+  return (unsigned)(b > 148 * 32 ? 148 * 32 : (b < 1 ? 1 : b));
+}
+
+cudaError_t launch_trig_pre(const double* x, long long n, long long L, long long k0, long long Q, double2* A,
+                            cudaStream_t st) {
+  note_launch(), trig_pre_kernel<<<ew_blocks(Q), 256, 0, st>>>(x, n, L, k0, Q, A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trig_mid(const double2* A2, const double2* H, long long Q, double2* A, cudaStream_t st) {
+  note_launch(), trig_mid_kernel<<<ew_blocks(Q), 256, 0, st>>>(A2, H, Q, A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trig_post(int kind, const double2* A2, long long n, long long L, long long k0, long long n0,
+                             long long Q, double* out, cudaStream_t st) {
+  note_launch(), trig_post_kernel<<<ew_blocks(n), 256, 0, st>>>(kind, A2, n, L, k0, n0, Q, out);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- launch
 static int pick_w(int N2) {
   int T = N2 >= 8 ? N2 / 8 : 1;

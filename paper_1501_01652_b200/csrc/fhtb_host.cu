@@ -57,6 +57,67 @@ int fail(int code, const std::string& msg) {
     }                                                                               \
   } while (0)
 
+// ------------------------------------------------ kernel-family timing
+// fhtb_set_option("kernel_timing", 1): CUDA events around every launch of the
+// apply scheduler, recorded on the stream the kernel runs on, together with
+// the algorithmic bytes the launch moves.  fhtb_kernel_times
+// reads and resets the per-family sums (bench.py roofline.kernels[]).
+enum KFam {
+  kfPass1, kfPass2, kfNarrow, kfRowdot, kfReduce, kfOnepass, kfNear, kfNearReduce,
+  kfChirp1, kfChirp2, kfChirp3, kfChirpReduce, kfOther, kNumFam
+};
+const char* const kFamNames[kNumFam] = {
+  "far_pass1", "far_pass2", "far_narrow_cols", "far_rowdot", "far_reduce", "far_onepass", "near",
+  "near_reduce", "chirp_pass1", "chirp_pass2", "chirp_pass3", "chirp_reduce", "other"};
+struct KtRec {
+  int fam, dev;
+  cudaEvent_t a, b;
+  double bytes;
+};
+std::mutex g_kt_mu;
+int g_kt_on = 0;
+std::vector<KtRec> g_kt;
+std::map<int, std::vector<cudaEvent_t>> g_kt_pool;
+
+cudaEvent_t kt_event(int dev) {
+  std::lock_guard<std::mutex> lk(g_kt_mu);
+  auto& p = g_kt_pool[dev];
+  if (!p.empty()) {
+    cudaEvent_t e = p.back();
+    p.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  return e;
+}
+
+struct KtScope {
+  int fam, dev = 0;
+  cudaStream_t st;
+  double bytes;
+  cudaEvent_t a = nullptr;
+  KtScope(int f, cudaStream_t s, double by) : fam(f), st(s), bytes(by) {
+    if (!g_kt_on) return;
+    cudaGetDevice(&dev);
+    a = kt_event(dev);
+    if (a && cudaEventRecord(a, st) != cudaSuccess) a = nullptr;
+  }
+  ~KtScope() {
+    if (!a) return;
+    cudaEvent_t b = kt_event(dev);
+    if (!b || cudaEventRecord(b, st) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lk(g_kt_mu);
+    g_kt.push_back(KtRec{fam, dev, a, b, bytes});
+  }
+};
+
+#define KT(fam, st, bytes, call)         \
+  do {                                   \
+    KtScope kt_((fam), (st), (bytes));   \
+    CU(call);                            \
+  } while (0)
+
 // ------------------------------------------------------------ host math
 // a_0..a_{count-1}(nu) by the ratio recurrence (bessel.py:45-58)
 std::vector<double> asy_coeffs(int nu, int count) {
@@ -504,6 +565,40 @@ int fhtb_abi_version(void) { return 1; }
 int64_t fhtb_launch_count(void) { return g_launches.load(); }
 const char* fhtb_last_error(void) { return g_err.c_str(); }
 
+int32_t fhtb_kernel_families(void) { return kNumFam; }
+
+const char* fhtb_kernel_family_name(int32_t i) { return (i >= 0 && i < kNumFam) ? kFamNames[i] : ""; }
+
+int fhtb_kernel_times(double* ms, double* bytes, int64_t* launches, int32_t n_fam) {
+  std::vector<KtRec> recs;
+  {
+    std::lock_guard<std::mutex> lk(g_kt_mu);
+    recs.swap(g_kt);
+  }
+  for (int i = 0; i < n_fam; ++i) {
+    if (ms) ms[i] = 0.0;
+    if (bytes) bytes[i] = 0.0;
+    if (launches) launches[i] = 0;
+  }
+  int rc = FHTB_OK;
+  for (const KtRec& r : recs) {
+    float t = 0.f;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) {
+      (void)cudaGetLastError();
+      rc = fail(FHTB_ECUDA, "kernel timing: event query failed");
+    }
+    if (r.fam < n_fam) {
+      if (ms) ms[r.fam] += t;
+      if (bytes) bytes[r.fam] += r.bytes;
+      if (launches) launches[r.fam] += 1;
+    }
+    std::lock_guard<std::mutex> lk(g_kt_mu);
+    g_kt_pool[r.dev].push_back(r.a);
+    g_kt_pool[r.dev].push_back(r.b);
+  }
+  return rc;
+}
+
 int fhtb_init(void) {
   DevCtx* c;
   return get_ctx(&c);
@@ -513,6 +608,10 @@ int fhtb_set_option(const char* key, int64_t value) {
   if (!key) return fail(FHTB_EINVAL, "null key");
   if (!std::strcmp(key, "far_prune")) {
     g_far_prune = (int)value;
+    return FHTB_OK;
+  }
+  if (!std::strcmp(key, "kernel_timing")) {
+    g_kt_on = value ? 1 : 0;
     return FHTB_OK;
   }
   if (!std::strcmp(key, "near_priority")) {
@@ -1352,6 +1451,49 @@ int run_exchange(const fhtb_grid* g, DevCtx* ctx, const std::vector<ReqDesc>& rs
   return FHTB_OK;
 }
 
+// Algorithmic bytes of one far-field chunk per kernel family (kernel timing;
+// the per-unit terms of fhtb_grid_far_model_bytes, restricted to this shard's
+// pairs): [0] the first launch (pass 1 / column tables / chirp pass 1 / one
+// pass), [1] the second (pass 2 / row sums / chirp pass 2), [2] chirp pass 3,
+// [3] the reduction into F.
+void chunk_bytes(const fhtb_grid* g, const FarPlan& fp, size_t ci, const std::vector<ReqDesc>& rs, int npairs,
+                 double out[4]) {
+  out[0] = out[1] = out[2] = out[3] = 0.0;
+  const int2 ch = fp.chunks[ci];
+  const double L = (double)g->L, np = (double)npairs;
+  int last_vec = -1;
+  for (int u = ch.x; u < ch.y; ++u) {
+    const UnitDesc& ud = fp.units[u];
+    const BlockDesc& x = g->bdesc[ud.block];
+    const double c0 = (double)std::max<long long>(x.c0, rs[ud.req].col_lo);
+    const double cols = std::max(0.0, (double)std::min(x.c1, g->n_data_cols + 1) - c0);
+    if (ud.vec != last_vec) out[3] += 16.0 * (double)g->n_out;       // F read + write per vector
+    last_vec = ud.vec;
+    if (!g->direct) {
+      const double Q = (double)(1LL << x.logQ), J = (double)x.J;
+      out[0] += 2.0 * np * 16.0 * Q + 8.0 * cols;
+      out[1] += 2.0 * np * 32.0 * Q;
+      out[2] += 2.0 * np * 16.0 * Q + 8.0 * J;
+      out[3] += 8.0 * (double)g->n_out;
+      continue;
+    }
+    const double rows = (double)std::max<long long>(0, x.r1 - x.r0);
+    out[3] += 8.0 * rows;
+    if (g->logN2 == 0) {
+      out[0] += 8.0 * cols + 8.0 * rows;
+    } else if (x.dmode == 1) {
+      const double l1 = (double)(1LL << x.dlogL1);
+      out[0] += 8.0 * cols + np * 16.0 * l1;                          // column table written
+      out[1] += np * 16.0 * l1 + 8.0 * rows;                          // read, partial row
+    } else {
+      out[0] += np * 32.0 * L + 8.0 * cols;                           // G written
+      double rd = 1.0;
+      if (x.dmode == 2) rd = std::min(1.0, 2.0 * (rows + 1) / (double)(1LL << (g->logQ - x.dlogL1)));
+      out[1] += np * 32.0 * L * rd + 8.0 * rows;                      // G read, partial row
+    }
+  }
+}
+
 int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, const double* C, int64_t ldc,
                int32_t n_vec, double* F, int64_t ldf, int32_t flags, int32_t shard, int32_t n_shards,
                const XCtx* xc, void* ws, size_t ws_bytes, void* stream, const HostPipe* hp) {
@@ -1465,8 +1607,8 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
     na.overwrite = 0;
     na.shard = shard;
     na.n_shards = n_shards;
-    CU(launch_near(na, (int)g->tiles.size(), (int)q0.size() - 1, max_cols, nst));
-    CU(launch_near_reduce(g->d_rts, (int)g->rts.size(), part, Fn, ldfn, n_vec, 0, nst));
+    KT(kfNear, nst, 0.0, launch_near(na, (int)g->tiles.size(), (int)q0.size() - 1, max_cols, nst));
+    KT(kfNearReduce, nst, 0.0, launch_near_reduce(g->d_rts, (int)g->rts.size(), part, Fn, ldfn, n_vec, 0, nst));
   }
   if (overlap) CU(cudaEventRecord(nax->ndone, nst));
 
@@ -1538,8 +1680,10 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
         a.logQ = g->logQ;
         a.vranges = d_ch;
         a.u0 = 0;
-        CU(launch_far_onepass(a, g->logN1, (int)nu, st));
-        CU(launch_far_reduce(a, (int)nu, st));
+        double cb[4];
+        chunk_bytes(g, fp, 0, rs, p1 - p0, cb);
+        KT(kfOnepass, st, cb[0], launch_far_onepass(a, g->logN1, (int)nu, st));
+        KT(kfReduce, st, cb[3], launch_far_reduce(a, (int)nu, st));
       } else {
         if (pipe && hp) {
           // the second aux stream and the reductions wait for the tables only
@@ -1557,6 +1701,8 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
           double2 *ql, *qh;
           int qb;
           if (int r = get_qtab(ctx, lq, &ql, &qh, &qb)) return r;
+          double cb[4];
+          chunk_bytes(g, fp, ci, rs, p1 - p0, cb);
           a.qlo = ql;
           a.qhi = qh;
           a.qbits = qb;
@@ -1579,24 +1725,24 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
               a.part = b ? part2 : part;
               if (ci >= 2) CU(cudaStreamWaitEvent(cs, ax->red[b], 0));
             }
-            if (mode != 1 && g_far_prefetch) CU(launch_prefetch_rows(a, n_units, cs));
+            if (mode != 1 && g_far_prefetch) KT(kfOther, cs, 0.0, launch_prefetch_rows(a, n_units, cs));
             if (mode == 1) {
-              CU(launch_far_colgen(a, l1, n_units, cs));
+              KT(kfNarrow, cs, cb[0] + cb[1], launch_far_colgen(a, l1, n_units, cs));
             } else if (mode == 2) {
-              CU(launch_far_pass1(a, l2, n_units, cs));
+              KT(kfPass1, cs, cb[0], launch_far_pass1(a, l2, n_units, cs));
               int kb = 1;
               for (int u = fp.chunks[ci].x; u < fp.chunks[ci].y; ++u)
                 kb = std::max(kb, g->bdesc[fp.units[u].block].kbins);
-              CU(launch_far_rowdot(a, n_units, kb, cs));
+              KT(kfRowdot, cs, cb[1], launch_far_rowdot(a, n_units, kb, cs));
             } else {
-              CU(launch_far_pass1(a, l2, n_units, cs));
-              CU(launch_far_pass2(a, l1, n_units, cs));
+              KT(kfPass1, cs, cb[0], launch_far_pass1(a, l2, n_units, cs));
+              KT(kfPass2, cs, cb[1], launch_far_pass2(a, l1, n_units, cs));
             }
             if (pipe) {
               CU(cudaEventRecord(ax->done[b], cs));
               CU(cudaStreamWaitEvent(st, ax->done[b], 0));
             }
-            CU(launch_far_reduce(a, n_units, st));
+            KT(kfReduce, st, cb[3], launch_far_reduce(a, n_units, st));
             if (pipe) CU(cudaEventRecord(ax->red[b], st));
           } else {
             int l1, l2;
@@ -1604,10 +1750,10 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
             a.L1 = 1 << l1;
             a.L2 = 1 << l2;
             CU(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)n_units * g->n_out, st));
-            CU(launch_chirp_pass1(a, l2, n_units, fp.chunk_key[ci], st));
-            CU(launch_chirp_pass2(a, l1, n_units, st));
-            CU(launch_chirp_pass3(a, l2, n_units, st));
-            CU(launch_chirp_reduce(a, n_units, st));
+            KT(kfChirp1, st, cb[0], launch_chirp_pass1(a, l2, n_units, fp.chunk_key[ci], st));
+            KT(kfChirp2, st, cb[1], launch_chirp_pass2(a, l1, n_units, st));
+            KT(kfChirp3, st, cb[2], launch_chirp_pass3(a, l2, n_units, st));
+            KT(kfChirpReduce, st, cb[3], launch_chirp_reduce(a, n_units, st));
           }
         }
       }
@@ -1616,7 +1762,7 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
 
   if (overlap) {
     CU(cudaStreamWaitEvent(st, nax->ndone, 0));
-    CU(launch_add_rows(F, ldf, Fn, ldfn, n_vec, g->n_out, st));
+    KT(kfOther, st, 0.0, launch_add_rows(F, ldf, Fn, ldfn, n_vec, g->n_out, st));
   }
   return FHTB_OK;
 }
@@ -1746,7 +1892,8 @@ static int trig_geom(int kind, int64_t n, long long* L, long long* k0, int* logQ
     return fail(FHTB_EINVAL, "kind must be DCT1 or DST1");
   }
   *logQ = std::max(1, ilog2ll(2 * n - 1));
-  if (*logQ > 13) return fail(FHTB_EINVAL, "trig_apply supports length <= 4096");
+  // Q <= 8192: one CTA per row; beyond, the multi-pass FFT (Q <= 2^26)
+  if (*logQ > 26) return fail(FHTB_EINVAL, "trig_apply supports length <= 2^25");
   return FHTB_OK;
 }
 
@@ -1755,7 +1902,7 @@ size_t fhtb_trig_workspace(int kind, int64_t length, int64_t batch) {
   long long L, k0;
   int lq;
   if (trig_geom(kind, length, &L, &k0, &lq)) return 0;
-  return 3 * align_up(sizeof(double2) << lq) + 4096;
+  return (lq > 13 ? 4 : 3) * align_up(sizeof(double2) << lq) + 4096;
 }
 
 int fhtb_trig_apply(int kind, int64_t length, const double* v, int64_t batch, double* out, void* ws,
@@ -1775,7 +1922,20 @@ int fhtb_trig_apply(int kind, int64_t length, const double* v, int64_t batch, do
   double2* H = cv.take<double2>(Q);
   CU(launch_chirp_filter(h, Q, length, length, 1, L, st));
   if (int r = plain_fft(ctx, lq, h, tmp, H, 0, st)) return r;
-  CU(launch_trig(kind, lq, length, L, k0, k0, v, out, batch, H, ctx->tw, st));
+  if (lq <= 13) {
+    CU(launch_trig(kind, lq, length, L, k0, k0, v, out, batch, H, ctx->tw, st));
+    return FHTB_OK;
+  }
+  double2* A = h;
+  double2* A2 = cv.take<double2>(Q);
+  if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small");
+  for (int64_t b = 0; b < batch; ++b) {
+    CU(launch_trig_pre(v + b * length, length, L, k0, Q, A, st));
+    if (int r = plain_fft(ctx, lq, A, tmp, A2, 0, st)) return r;
+    CU(launch_trig_mid(A2, H, Q, A, st));
+    if (int r = plain_fft(ctx, lq, A, tmp, A2, 0, st)) return r;
+    CU(launch_trig_post(kind, A2, length, L, k0, k0, Q, out + b * length, st));
+  }
   return FHTB_OK;
 }
 

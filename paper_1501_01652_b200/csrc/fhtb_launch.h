@@ -120,6 +120,12 @@ cudaError_t launch_plain_fft(const FarArgs& a, int logN1, int logN2, const doubl
                              double2* out, int transposed, cudaStream_t st);
 cudaError_t launch_trig(int kind, int logQ, long long n, long long L, long long k0, long long n0, const double* v,
                         double* out, long long batch, const double2* H, const double2* tw, cudaStream_t st);
+// trig lengths with Q > 8192: elementwise stages around plain_fft
+cudaError_t launch_trig_pre(const double* x, long long n, long long L, long long k0, long long Q, double2* A,
+                            cudaStream_t st);
+cudaError_t launch_trig_mid(const double2* A2, const double2* H, long long Q, double2* A, cudaStream_t st);
+cudaError_t launch_trig_post(int kind, const double2* A2, long long n, long long L, long long k0, long long n0,
+                             long long Q, double* out, cudaStream_t st);
 
 // utilities
 cudaError_t launch_twiddles(double2* tw_pool, int max_log, cudaStream_t st);

@@ -1,0 +1,192 @@
+"""BASELINE.json full-size configurations pinned to the REFERENCE
+(tests/golden/make_fullsize.py ran the reference package in the build
+container and stored sampled rows):
+
+* `fast`:   the reference's own fast transform (schlomilch_fast,
+            fourier_bessel_eval, dht) at those rows -- the north star's
+            "match the reference CPU implementation within 10 eps ||c||_1";
+* `direct`: direct fp64 sums sum_n c_n J_nu(r_k omega_n) at those rows with
+            the reference's bessel_j (and _rows_direct for the DHT), i.e.
+            independent of the CUDA Bessel evaluator that the GPU near field
+            and GPU direct kernel share.
+
+Inputs are regenerated here from the same numpy PCG64 seed words.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1501_01652_b200 as fh
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SEED, TASK_SEED = 1501, 1508
+
+
+@pytest.fixture(scope="module")
+def fx():
+    with open(os.path.join(HERE, "golden", "fullsize.json")) as f:
+        meta = json.load(f)
+    arr = np.load(os.path.join(HERE, "golden", "fullsize.npz"))
+    return meta, arr
+
+
+def cfg2_vector(n, b=0):
+    return np.random.default_rng([SEED, n, b]).standard_normal(n) / np.arange(1, n + 1, dtype=float)
+
+
+def task_vector(kind, n, b=0):
+    g = np.random.default_rng([TASK_SEED, n, b])
+    return g.uniform(-1.0, 1.0, n) if kind == "u" else g.standard_normal(n)
+
+
+def sweep_vector(n):
+    return np.random.default_rng([SEED, n, 9]).standard_normal(n)
+
+
+def _check(got, want, tol, what):
+    err = np.atleast_1d(np.abs(np.asarray(got) - np.asarray(want)))
+    i = int(np.argmax(err))
+    assert err[i] <= tol, "%s: max err %.3e at %d > tol %.3e" % (what, err[i], i, tol)
+    return float(err[i])
+
+
+@pytest.mark.parametrize("eps", [1e-3, 1e-8, 1e-15])
+def test_cfg2_vs_reference(cuda_dev, fx, eps):
+    """cfg2 (nu=4, gamma=4, N=2^20) at every eps: reference schlomilch_fast
+    rows, and reference direct sums."""
+    meta, arr = fx
+    n = 2 ** 20
+    c = cfg2_vector(n)
+    C = torch.from_numpy(c).to(cuda_dev)
+    F = fh.schlomilch_fast(fh.select_params(4, n, eps, gamma=4.0), C).cpu().numpy()
+    key = "cfg2_eps" + {1e-3: "1e-3", 1e-8: "1e-8", 1e-15: "1e-15"}[eps]
+    assert meta[key]["l1"] == pytest.approx(np.abs(c).sum(), rel=1e-12)   # same inputs
+    tol = 10 * eps * np.abs(c).sum()
+    rows = arr[key + "/rows"]
+    _check(F[rows - 1], arr[key + "/fast"], tol, "vs reference fast")
+    rows = arr["cfg2_direct/rows"]
+    _check(F[rows - 1], arr["cfg2_direct/direct"], tol, "vs reference direct")
+
+
+def test_fb_cfg3_vs_reference(cuda_dev, fx):
+    meta, arr = fx
+    n, eps = 2 ** 18, 1e-12
+    c = task_vector("u", n)
+    F = fh.fourier_bessel_eval(0, torch.from_numpy(c).to(cuda_dev), eps).cpu().numpy()
+    tol = 10 * eps * np.abs(c).sum()
+    rows = arr["fb_cfg3/rows"]
+    _check(F[rows - 1], arr["fb_cfg3/fast"], tol, "vs reference fourier_bessel_eval")
+    _check(F[rows - 1], arr["fb_cfg3/direct"], tol, "vs reference direct")
+
+
+def test_dht_cfg4_vs_reference(cuda_dev, fx):
+    meta, arr = fx
+    n, eps = 2 ** 16, 1e-15
+    c = task_vector("n", n)
+    plan = fh.dht_plan(n, eps)
+    st = {}
+    F = fh.dht(plan, torch.from_numpy(c).to(cuda_dev), stats=st).cpu().numpy()
+    tol = 10 * eps * np.abs(c).sum()
+    if "dht_cfg4_fast/full" in arr.files:
+        _check(F, arr["dht_cfg4_fast/full"], tol, "vs reference dht (whole vector)")
+        for k, v in meta["dht_cfg4_fast"]["stats"].items():
+            assert st.get(k) == v, (k, st.get(k), v)
+    rows = arr["dht_cfg4_direct/rows"]
+    _check(F[rows - 1], arr["dht_cfg4_direct/direct"], tol, "vs reference _rows_direct")
+
+
+@pytest.mark.parametrize("key", ["dht_4096_eps1e-15", "dht_16384_eps1e-8"])
+def test_dht_whole_vector_vs_reference(cuda_dev, fx, key):
+    meta, arr = fx
+    m = meta[key]
+    n, eps = m["n"], m["eps"]
+    c = sweep_vector(n)
+    F = fh.dht(fh.dht_plan(n, eps), torch.from_numpy(c).to(cuda_dev)).cpu().numpy()
+    _check(F, arr[key + "/full"], 10 * eps * np.abs(c).sum(), key)
+
+
+@pytest.mark.parametrize("key", ["schl_2^18_eps1e-3", "schl_2^18_eps1e-8", "schl_2^18_eps1e-15",
+                                 "schl_2^20_eps1e-15"])
+def test_schlomilch_sweep_vs_reference_fast(cuda_dev, fx, key):
+    meta, arr = fx
+    m = meta[key]
+    n, eps = m["n"], m["eps"]
+    c = sweep_vector(n)
+    F = fh.schlomilch_fast(fh.select_params(0, n, eps), torch.from_numpy(c).to(cuda_dev)).cpu().numpy()
+    rows = arr[key + "/rows"]
+    _check(F[rows - 1], arr[key + "/fast"], 10 * eps * np.abs(c).sum(), key)
+
+
+@pytest.mark.parametrize("lg", [18, 20, 22, 24])
+@pytest.mark.parametrize("eps", [1e-3, 1e-8, 1e-15])
+def test_schlomilch_sweep_vs_reference_direct(cuda_dev, fx, lg, eps):
+    """BASELINE configs[4] Schlomilch nu=0 at N=2^18..2^24, every eps, against
+    direct sums of the reference's bessel_j (arguments up to ~5e7)."""
+    meta, arr = fx
+    n = 2 ** lg
+    key = "schl_2^%d_direct" % lg
+    c = sweep_vector(n)
+    F = fh.schlomilch_fast(fh.select_params(0, n, eps), torch.from_numpy(c).to(cuda_dev)).cpu().numpy()
+    rows = arr[key + "/rows"]
+    _check(F[rows - 1], arr[key + "/direct"], 10 * eps * np.abs(c).sum(), key)
+
+
+@pytest.mark.parametrize("lg,eps", [(18, 1e-3), (18, 1e-8), (18, 1e-15), (20, 1e-15), (20, 1e-3),
+                                    (22, 1e-8), (24, 1e-3)])
+def test_dht_sweep_vs_reference_direct(cuda_dev, fx, lg, eps):
+    """BASELINE configs[4] DHT at N=2^18..2^24 against direct sums of the
+    reference's bessel_j at roots from the reference's Newton iteration
+    (without its 1e-13 residual gate, which fp64 cannot meet beyond ~2e6)."""
+    meta, arr = fx
+    n = 2 ** lg
+    key = "dht_2^%d_direct" % lg
+    c = sweep_vector(n)
+    F = fh.dht(fh.dht_plan(n, eps), torch.from_numpy(c).to(cuda_dev)).cpu().numpy()
+    rows = arr[key + "/rows"]
+    _check(F[rows - 1], arr[key + "/direct"], 10 * eps * np.abs(c).sum(), key)
+
+
+def test_bessel_large_arguments_vs_reference(cuda_dev, fx):
+    """J_nu at arguments up to 4.2e6 in every dispatch range (Taylor, Miller,
+    Hankel; both sides of each cutoff) -- the range the near field and direct
+    kernels evaluate at N = 2^20..2^24.  Against the reference within 2e-15
+    plus the reference's own phase rounding (ulp(z)/2 rad times the envelope
+    sqrt(2/(pi z)), bessel.py:72-91), and against 30-digit mpmath values
+    within 2e-15 outright."""
+    meta, arr = fx
+    for o in meta["bessel_large"]["orders"]:
+        nu = o["nu"]
+        z = arr["bessel_large/z_%d" % nu]
+        want = arr["bessel_large/j_%d" % nu]
+        got = fh.bessel_j(nu, z)
+        env = np.sqrt(2.0 / (np.pi * np.maximum(z, 1.0)))
+        tol = 2e-15 + np.where(z >= o["s_hi"], np.spacing(z) * env, 0.0)
+        bad = np.abs(got - want) > tol
+        assert not bad.any(), (nu, z[bad][:5], (got - want)[bad][:5])
+    for nu in meta["bessel_mp"]["orders"]:
+        z = arr["bessel_mp/z_%d" % nu]
+        _check(fh.bessel_j(nu, z), arr["bessel_mp/j_%d" % nu], 2e-15, "J_%d vs mpmath" % nu)
+
+
+def test_trig_any_length_vs_reference(cuda_dev, fx):
+    """trig.apply beyond 4096 (trig.py:80-92 takes any length; the reference
+    applies N+-1 up to 2^20+-1, schlomilch.py:269-270): sampled outputs and a
+    checksum w . out against the reference's pocketfft result."""
+    meta, arr = fx
+    for case in meta["trig"]["cases"]:
+        kind, n, b = case["kind"], case["n"], case["batch"]
+        key = "trig/%s_%d" % (kind, n)
+        v = np.random.default_rng([77, n, kind == fh.DST1]).standard_normal((b, n))
+        w = np.random.default_rng([78, n]).standard_normal(n)
+        out = fh.apply(fh.make_plan(n, kind), v)
+        l1 = arr[key + "_l1"]
+        idx = arr[key + "_idx"]
+        for r in range(b):
+            _check(out[r, idx], arr[key + "_val"][r], 1e-13 * l1[r], "%s %d row %d" % (kind, n, r))
+            _check(out[r] @ w, arr[key + "_chk"][r], 1e-13 * l1[r] * np.abs(w).sum(), "%s %d checksum" % (kind, n))
