@@ -42,7 +42,10 @@ int64_t fhtb_launch_count(void);
  * current device.  Idempotent; synchronous. */
 int fhtb_init(void);
 /* Tunables: "far_chunk_bytes" (two-pass intermediate budget), ...;
- * "kernel_timing" 1/0 turns on CUDA-event timing of every apply launch. */
+ * "kernel_timing" 1/0 turns on CUDA-event timing of every apply launch;
+ * "serial" 1/0 issues every launch on the caller's stream in plan order (no
+ * chunk pipeline, near field after the far field) so that those per-launch
+ * times are exclusive.  Results are bit-identical either way. */
 int fhtb_set_option(const char* key, int64_t value);
 /* Kernel-family timing (no reference counterpart; bench.py roofline):
  * with "kernel_timing" on, every far/near launch of fhtb_apply* is bracketed

@@ -36,6 +36,7 @@ int g_far_prune = 1;                       // pruned side blocks (direct two-pas
 int g_near_split = 1;                      // near field: order-parity classes
 int g_far_streams = 2;                     // far-field chunks in flight (direct two-pass)
 int g_near_overlap = 1;                    // near field on its own stream beside the far field
+int g_serial = 0;                          // diagnostics: every launch on the caller's stream, in order
 int g_prune_rows = 11;                     // narrow-row blocks: rows below 2^g_prune_rows
 int g_rowdot_bins = 1;                     // narrow-row blocks: at most this many pass-2 bins per column
 int g_min_lc = 9;                          // narrow-column blocks: smallest column FFT 2^g_min_lc
@@ -612,6 +613,10 @@ int fhtb_set_option(const char* key, int64_t value) {
   }
   if (!std::strcmp(key, "kernel_timing")) {
     g_kt_on = value ? 1 : 0;
+    return FHTB_OK;
+  }
+  if (!std::strcmp(key, "serial")) {
+    g_serial = value ? 1 : 0;
     return FHTB_OK;
   }
   if (!std::strcmp(key, "near_priority")) {
@@ -1526,7 +1531,7 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
   // an auxiliary stream into a separate buffer Fn, added to F at the end on
   // the caller's stream (F = far sum + near sum, as in the serial order).
   const bool overlap = (flags & FHTB_NEAR) && (flags & FHTB_FAR) && !g->tiles.empty() &&
-                       !g->blocks.empty() && g_near_overlap;
+                       !g->blocks.empty() && g_near_overlap && !g_serial;
   cudaStream_t nst = st;
   double* Fn = F;
   int64_t ldfn = ldf;
@@ -1629,7 +1634,7 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
       double2* G = fp.g_bytes ? (double2*)cv.take<char>(fp.g_bytes) : nullptr;
       double* part = fp.part_bytes ? (double*)cv.take<char>(fp.part_bytes) : nullptr;
       // second buffer set: two chunks in flight on two streams (direct two-pass)
-      const bool pipe = g->direct && g->logN2 > 0 && g_far_streams > 1 && fp.chunks.size() > 1;
+      const bool pipe = g->direct && g->logN2 > 0 && g_far_streams > 1 && fp.chunks.size() > 1 && !g_serial;
       double2* G2 = (pipe && fp.g_bytes) ? (double2*)cv.take<char>(fp.g_bytes) : nullptr;
       double* part2 = (pipe && fp.part_bytes) ? (double*)cv.take<char>(fp.part_bytes) : nullptr;
       if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small");
