@@ -36,6 +36,13 @@ extern "C" {
 
 int fhtb_abi_version(void);
 const char* fhtb_last_error(void);
+/* Non-finite outputs (reference contract: cli.py:128-130, exit code 3 when the
+ * output holds a non-finite value).  Every kernel that writes final values to
+ * F (far/chirp reductions, near-field reduction and add) sets a per-device
+ * flag when it writes inf or NaN.  fhtb_nonfinite_check synchronises `stream`
+ * on the current device, clears the flag and returns FHTB_ENONFINITE if it
+ * was set since the previous check (FHTB_OK otherwise). */
+int fhtb_nonfinite_check(void* stream);
 /* Cumulative number of CUDA kernels this library has launched (all devices). */
 int64_t fhtb_launch_count(void);
 /* Prepare per-device tables (twiddles, Bessel order constants) on the

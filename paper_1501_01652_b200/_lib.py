@@ -50,6 +50,7 @@ EXPORTS = {
     "fhtb_abi_version": (i32, []),
     "fhtb_last_error": (ctypes.c_char_p, []),
     "fhtb_launch_count": (i64, []),
+    "fhtb_nonfinite_check": (i32, [vp]),
     "fhtb_init": (i32, []),
     "fhtb_set_option": (i32, [ctypes.c_char_p, i64]),
     "fhtb_kernel_families": (i32, []),
@@ -109,7 +110,7 @@ def load(path=LIB_PATH):
                              ("FHTB_NEAR_CHUNK_COLS_MULTI", b"near_chunk_cols_multi"), ("FHTB_NEAR_SPLIT", b"near_split"), ("FHTB_FAR_STREAMS", b"far_streams"),
                              ("FHTB_NEAR_OVERLAP", b"near_overlap"),
                              ("FHTB_FAR_PRUNE_ROWS", b"far_prune_rows"), ("FHTB_FAR_MIN_COLS", b"far_min_cols"),
-                             ("FHTB_FAR_ROWDOT_BINS", b"far_rowdot_bins"), ("FHTB_HOST_TAPER", b"host_taper"),
+                             ("FHTB_FAR_ROWDOT_BINS", b"far_rowdot_bins"), ("FHTB_FAR_ROWSUM", b"far_rowsum"), ("FHTB_HOST_TAPER", b"host_taper"),
                              ("FHTB_FAR_PREFETCH", b"far_prefetch"), ("FHTB_NEAR_PRIORITY", b"near_priority")):
                 if os.environ.get(env):
                     lib.fhtb_set_option(key, int(os.environ[env]))

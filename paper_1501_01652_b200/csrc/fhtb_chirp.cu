@@ -296,6 +296,7 @@ __global__ void chirp_reduce_kernel(FarArgs a, int n_units) {
       ++u;
     }
     *f = s;
+    if (!isfinite(s)) *a.nf = 1;
   }
 }
 

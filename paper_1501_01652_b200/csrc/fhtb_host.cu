@@ -38,6 +38,7 @@ int g_far_streams = 2;                     // far-field chunks in flight (direct
 int g_near_overlap = 1;                    // near field on its own stream beside the far field
 int g_serial = 0;                          // diagnostics: every launch on the caller's stream, in order
 int g_prune_rows = 11;                     // narrow-row blocks: rows below 2^g_prune_rows
+int g_rowsum = 1;                          // narrow-row blocks: fully fused form (dmode 3) where it applies
 int g_rowdot_bins = 1;                     // narrow-row blocks: at most this many pass-2 bins per column
 int g_min_lc = 9;                          // narrow-column blocks: smallest column FFT 2^g_min_lc
 int g_near_priority = 0;                   // near-field stream priority (see get_aux)
@@ -65,11 +66,12 @@ int fail(int code, const std::string& msg) {
 // reads and resets the per-family sums (bench.py roofline.kernels[]).
 enum KFam {
   kfPass1, kfPass2, kfNarrow, kfRowdot, kfReduce, kfOnepass, kfNear, kfNearReduce,
-  kfChirp1, kfChirp2, kfChirp3, kfChirpReduce, kfOther, kNumFam
+  kfChirp1, kfChirp2, kfChirp3, kfChirpReduce, kfOther, kfRowsum, kfRowsumFin, kNumFam
 };
 const char* const kFamNames[kNumFam] = {
   "far_pass1", "far_pass2", "far_narrow_cols", "far_rowdot", "far_reduce", "far_onepass", "near",
-  "near_reduce", "chirp_pass1", "chirp_pass2", "chirp_pass3", "chirp_reduce", "other"};
+  "near_reduce", "chirp_pass1", "chirp_pass2", "chirp_pass3", "chirp_reduce", "other", "far_rowsum",
+  "far_rowsum_fin"};
 struct KtRec {
   int fam, dev;
   cudaEvent_t a, b;
@@ -178,6 +180,7 @@ struct DevCtx {
   double2* tw = nullptr;           // twiddle pool, N = 2..8192
   JOrder* jtab = nullptr;          // orders 0..kMaxOrder
   unsigned long long* scratch = nullptr;
+  int* nf = nullptr;               // set to 1 by any reduction that writes a non-finite output
   std::map<int, std::pair<double2*, double2*>> qtab;   // four-step twiddles per log2 Q
 };
 
@@ -241,6 +244,8 @@ int get_ctx(DevCtx** out) {
   CU(cudaMalloc(&c.jtab, tab.size() * sizeof(JOrder)));
   CU(cudaMemcpy(c.jtab, tab.data(), tab.size() * sizeof(JOrder), cudaMemcpyHostToDevice));
   CU(cudaMalloc(&c.scratch, 64));
+  CU(cudaMalloc(&c.nf, sizeof(int)));
+  CU(cudaMemset(c.nf, 0, sizeof(int)));
   CU(cudaDeviceSynchronize());
   g_ctx[dev] = c;
   *out = &g_ctx[dev];
@@ -548,6 +553,7 @@ int plain_fft(DevCtx* ctx, int logQ, const double2* in, double2* tmp, double2* o
   a.L1 = 1 << l1;
   a.L2 = 1 << l2;
   a.tw = ctx->tw;
+  a.nf = ctx->nf;
   double2 *ql, *qh;
   int qb;
   if (int r = get_qtab(ctx, logQ, &ql, &qh, &qb)) return r;
@@ -605,6 +611,17 @@ int fhtb_init(void) {
   return get_ctx(&c);
 }
 
+int fhtb_nonfinite_check(void* stream) {
+  DevCtx* c;
+  if (int r = get_ctx(&c)) return r;
+  int flag = 0;
+  CU(cudaMemcpyAsync(&flag, c->nf, sizeof(int), cudaMemcpyDeviceToHost, S(stream)));
+  CU(cudaMemsetAsync(c->nf, 0, sizeof(int), S(stream)));
+  CU(cudaStreamSynchronize(S(stream)));
+  if (flag) return fail(FHTB_ENONFINITE, "non-finite values in output");
+  return FHTB_OK;
+}
+
 int fhtb_set_option(const char* key, int64_t value) {
   if (!key) return fail(FHTB_EINVAL, "null key");
   if (!std::strcmp(key, "far_prune")) {
@@ -630,6 +647,10 @@ int fhtb_set_option(const char* key, int64_t value) {
   if (!std::strcmp(key, "host_taper")) {
     if (value < 1 || value > 64) return fail(FHTB_EINVAL, "host_taper must be 1..64");
     g_host_taper = (int)value;
+    return FHTB_OK;
+  }
+  if (!std::strcmp(key, "far_rowsum")) {
+    g_rowsum = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2));
     return FHTB_OK;
   }
   if (!std::strcmp(key, "far_rowdot_bins")) {
@@ -860,6 +881,20 @@ int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
         x.dmode = 2;                 // narrow rows with a longer pass-1 FFT, one bin
         x.dlogL1 = g->logQ - lr;
       }
+      // narrow rows, fully fused (far_rowsum_kernel): column FFTs of
+      // 2^ls >= r1 points (128..4096), pairs folded per column, no
+      // intermediate.  Needs r1 <= 2^ls < L and at least 16 columns n1.
+      const int ls = std::max(7, ilog2ll(std::max<long long>(x.r1, 2)));
+      // g_rowsum 1: only where the block would otherwise run the full pass 1 + pass 2
+      // (measured on cfg2: 17.3 vs 25.2 us per unit and pair at 4096 points; the
+      // 1024- and 128-point shapes lose to pass 1 + row sums, 14.7 / 26 vs 13.5 us);
+      // 2: every narrow-row block
+      if (g_far_prune && g_rowsum && (x.dmode == 0 || (x.dmode == 2 && g_rowsum >= 2)) && ls <= 12 &&
+          g->logQ - ls >= 4 && (1LL << ls) < g->L) {
+        x.dmode = 3;
+        x.dlogL1 = g->logQ - ls;
+        x.kbins = 1;
+      }
     }
     g->bdesc.push_back(x);
   }
@@ -917,6 +952,8 @@ double fhtb_grid_far_model_bytes(const fhtb_grid* g) {
     } else if (x.dmode == 2) {
       const double L2 = (double)(1LL << (g->logQ - x.dlogL1));
       bytes += terms * 16.0 * L * (1.0 + std::min(1.0, 2.0 * (rows + 1) / L2));
+    } else if (x.dmode == 3) {
+      bytes += 2.0 * 32.0 * rows * (double)(1LL << x.dlogL1);   // folded rows P written and read
     }                                                       // dmode 1: no intermediate
   }
   return bytes;
@@ -939,6 +976,12 @@ void fhtb_grid_destroy(fhtb_grid* g) {
 namespace {
 
 // bytes of intermediate per far-field unit
+// rows of a fused narrow-row block: k in [max(r0, 1), min(r1, L2))
+long long fused_rows(const fhtb_grid* g, const BlockDesc& x, int logL1) {
+  const long long L2 = 1LL << (g->logQ - logL1);
+  return std::max<long long>(1, std::min(x.r1, L2) - std::max<long long>(x.r0, 1));
+}
+
 size_t unit_bytes_q(const fhtb_grid* g, int logQ) {
   return (size_t)(g->direct ? g->M : 2 * g->M) * ((size_t)1 << logQ) * sizeof(double2);
 }
@@ -1001,8 +1044,15 @@ void plan_far(const fhtb_grid* g, const std::vector<ReqDesc>& rs, FarPlan& fp, i
         if (keys[i] == key) fp.units.push_back(all[i]);
       const long long n = (long long)fp.units.size() - start;
       // narrow-column units keep only their column table (M x L1)
-      const size_t ub = (key / 64 == 1) ? (size_t)g->M * ((size_t)1 << (key % 64)) * sizeof(double2)
-                                        : unit_bytes_q(g, g->logQ);
+      size_t ub = (key / 64 == 1) ? (size_t)g->M * ((size_t)1 << (key % 64)) * sizeof(double2)
+                                  : unit_bytes_q(g, g->logQ);
+      if (key / 64 == 3) {
+        // fused narrow rows: P[unit][A|B][rows][L1], rows = the widest block of the group
+        long long rs = 1;
+        for (size_t i = 0; i < all.size(); ++i)
+          if (keys[i] == key) rs = std::max(rs, fused_rows(g, g->bdesc[all[i].block], key % 64));
+        ub = 2 * (size_t)rs * ((size_t)1 << (key % 64)) * sizeof(double2);
+      }
       const long long cu = chunk_for(ub + pb, n);
       for (long long u0 = 0; u0 < n; u0 += cu) {
         fp.chunks.push_back(make_int2((int)(start + u0), (int)(start + std::min(n, u0 + cu))));
@@ -1282,6 +1332,8 @@ int fhtb_apply_host(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req,
   cudaStream_t st = S(stream);
   HostAux* hx;
   if (int r = get_haux(st, &hx)) return r;
+  DevCtx* ctx;
+  if (int r = get_ctx(&ctx)) return r;
   const int G = std::max(1, std::min({(int)n_groups, (int)n_vec, kMaxHostGroups}));
   // tapered groups: the first group's copy-in and the last group's copy-out
   // are the exposed parts, so those two groups get 1/host_taper of the share
@@ -1350,7 +1402,7 @@ int fhtb_apply_host(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req,
     CU(cudaStreamWaitEvent(hx->d2h, hx->fin[i], 0));
     if (near) {
       CU(cudaStreamWaitEvent(hx->d2h, hx->ndone, 0));
-      if (far) CU(launch_add_rows(Fg, ldf, Fn + (size_t)v0[i] * ldf, ldf, nv, ldf, hx->d2h));
+      if (far) CU(launch_add_rows(Fg, ldf, Fn + (size_t)v0[i] * ldf, ldf, nv, ldf, ctx->nf, hx->d2h));
     }
     CU(cudaMemcpy2DAsync(F_host + (size_t)v0[i] * ldf_host, ldf_host * sizeof(double), Fg, ldf * sizeof(double),
                          ldf * sizeof(double), nv, cudaMemcpyDeviceToHost, hx->d2h));
@@ -1414,6 +1466,7 @@ int run_exchange(const fhtb_grid* g, DevCtx* ctx, const std::vector<ReqDesc>& rs
   a.F = F;
   a.ldf = ldf;
   a.tw = ctx->tw;
+  a.nf = ctx->nf;
   a.part = part;
   a.part_stride = g->n_out;
   a.cs_tab = g->cs_tab;
@@ -1490,6 +1543,10 @@ void chunk_bytes(const fhtb_grid* g, const FarPlan& fp, size_t ci, const std::ve
       const double l1 = (double)(1LL << x.dlogL1);
       out[0] += 8.0 * cols + np * 16.0 * l1;                          // column table written
       out[1] += np * 16.0 * l1 + 8.0 * rows;                          // read, partial row
+    } else if (x.dmode == 3) {
+      const double l1 = (double)(1LL << x.dlogL1);
+      out[0] += 8.0 * cols + 32.0 * rows * l1;                        // folded rows written
+      out[1] += 32.0 * rows * l1 + 8.0 * rows;                        // read, partial row
     } else {
       out[0] += np * 32.0 * L + 8.0 * cols;                           // G written
       double rd = 1.0;
@@ -1596,6 +1653,7 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
       if (g->orders[i] != i) na.orders_identity = 0;
     }
     na.jtab = ctx->jtab;
+    na.nf = ctx->nf;
     na.reqs = split ? d_nreq : d_req;
     na.grp_q0 = d_q0;
     na.grp_v0 = d_v0;
@@ -1613,7 +1671,7 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
     na.shard = shard;
     na.n_shards = n_shards;
     KT(kfNear, nst, 0.0, launch_near(na, (int)g->tiles.size(), (int)q0.size() - 1, max_cols, nst));
-    KT(kfNearReduce, nst, 0.0, launch_near_reduce(g->d_rts, (int)g->rts.size(), part, Fn, ldfn, n_vec, 0, nst));
+    KT(kfNearReduce, nst, 0.0, launch_near_reduce(g->d_rts, (int)g->rts.size(), part, Fn, ldfn, n_vec, 0, ctx->nf, nst));
   }
   if (overlap) CU(cudaEventRecord(nax->ndone, nst));
 
@@ -1671,6 +1729,7 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
       a.F = F;
       a.ldf = ldf;
       a.tw = ctx->tw;
+  a.nf = ctx->nf;
       a.G = G;
       a.part = part;
       a.part_stride = g->n_out;
@@ -1733,6 +1792,13 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
             if (mode != 1 && g_far_prefetch) KT(kfOther, cs, 0.0, launch_prefetch_rows(a, n_units, cs));
             if (mode == 1) {
               KT(kfNarrow, cs, cb[0] + cb[1], launch_far_colgen(a, l1, n_units, cs));
+            } else if (mode == 3) {
+              long long rs = 1;
+              for (int u = fp.chunks[ci].x; u < fp.chunks[ci].y; ++u)
+                rs = std::max(rs, fused_rows(g, g->bdesc[fp.units[u].block], l1));
+              a.rs = (int)rs;
+              KT(kfRowsum, cs, cb[0], launch_far_rowsum(a, l2, n_units, cs));
+              KT(kfRowsumFin, cs, cb[1], launch_far_rowsum_fin(a, n_units, cs));
             } else if (mode == 2) {
               KT(kfPass1, cs, cb[0], launch_far_pass1(a, l2, n_units, cs));
               int kb = 1;
@@ -1767,7 +1833,7 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
 
   if (overlap) {
     CU(cudaStreamWaitEvent(st, nax->ndone, 0));
-    KT(kfOther, st, 0.0, launch_add_rows(F, ldf, Fn, ldfn, n_vec, g->n_out, st));
+    KT(kfOther, st, 0.0, launch_add_rows(F, ldf, Fn, ldfn, n_vec, g->n_out, ctx->nf, st));
   }
   return FHTB_OK;
 }
@@ -1862,6 +1928,7 @@ int fhtb_direct_apply(const fhtb_direct_desc* d, const fhtb_request* reqs, int32
     if (d->orders[i] != i) na.orders_identity = 0;
   }
   na.jtab = ctx->jtab;
+    na.nf = ctx->nf;
   na.reqs = d_req;
   na.grp_q0 = d_q0;
   na.grp_v0 = d_v0;
@@ -1876,7 +1943,7 @@ int fhtb_direct_apply(const fhtb_direct_desc* d, const fhtb_request* reqs, int32
   na.part_stride = (long long)n_vec * kNearRT;
   na.overwrite = (flags & FHTB_OVERWRITE) ? 1 : 0;
   CU(launch_near(na, (int)tiles.size(), (int)q0.size() - 1, max_cols, st));
-  CU(launch_near_reduce(d_rts, (int)rts.size(), part, F, ldf, n_vec, na.overwrite, st));
+  CU(launch_near_reduce(d_rts, (int)rts.size(), part, F, ldf, n_vec, na.overwrite, ctx->nf, st));
   return FHTB_OK;
 }
 

@@ -43,6 +43,7 @@ struct NearArgs {
   long long part_stride;         // n_vec * 64 doubles per partial slot
   int overwrite;
   int shard, n_shards;          // tiles t with t % n_shards == shard are computed
+  int* nf;                      // device flag: a non-finite value was written to F
 };
 
 struct FarArgs {
@@ -82,6 +83,8 @@ struct FarArgs {
   long long xn1, xchunk;
   const int2* xrow;
   const double2* xin;
+  int* nf;                      // device flag: a non-finite value was written to F
+  int rs;                       // fused narrow rows: row stride of P = G[unit][A|B][rs][L1]
 };
 cudaError_t launch_col_tables(double* w0, double* iw, long long L, double gamma, cudaStream_t st);
 
@@ -90,10 +93,10 @@ extern int g_chirp_variant;       // tuning knob for the chirp-z passes
 
 cudaError_t launch_near(const NearArgs& a, int n_tiles, int n_groups, int max_cols, cudaStream_t st);
 cudaError_t launch_add_rows(double* F, long long ldf, const double* Fn, long long ldn, int n_vec, long long n,
-                            cudaStream_t st);
+                            int* nf, cudaStream_t st);
 constexpr int kNearMaxCols = 128;   // request columns per near-field CTA (largest tile)
 cudaError_t launch_near_reduce(const NearRowTile* rt, int n_rt, const double* part, double* F,
-                               long long ldf, int n_vec, int overwrite, cudaStream_t st);
+                               long long ldf, int n_vec, int overwrite, int* nf, cudaStream_t st);
 constexpr int kNearRT = 64;
 
 // direct mode (2L power of two, unit-stride rows)
@@ -105,6 +108,8 @@ cudaError_t launch_far_pass2x_range(const FarArgs& a, int logN1, int n_pairs, in
 cudaError_t launch_far_reduce(const FarArgs& a, int n_units, cudaStream_t st);
 cudaError_t launch_far_colgen(const FarArgs& a, int logN1, int n_units, cudaStream_t st);
 cudaError_t launch_far_rowdot(const FarArgs& a, int n_units, int kbins, cudaStream_t st);
+cudaError_t launch_far_rowsum(const FarArgs& a, int logN2, int n_units, cudaStream_t st);
+cudaError_t launch_far_rowsum_fin(const FarArgs& a, int n_units, cudaStream_t st);
 cudaError_t launch_prefetch_rows(const FarArgs& a, int n_units, cudaStream_t st);
 cudaError_t launch_cs_table(double2* cs, long long L, double gamma, double pi_over_L, cudaStream_t st);
 

@@ -236,34 +236,38 @@ near_kernel(NearArgs a) {
       a.part[tile.part * a.part_stride + (long long)vec * kRT + i] = s;
     } else {
       double* dst = a.F + (long long)vec * a.ldf + j;
-      *dst = a.overwrite ? s : *dst + s;
+      s = a.overwrite ? s : *dst + s;
+      *dst = s;
+      if (!isfinite(s)) *a.nf = 1;
     }
   }
 }
 
 // F[v][j] += Fn[v][j]
 __global__ void add_rows_kernel(double* F, long long ldf, const double* Fn, long long ldn, int n_vec,
-                                long long n) {
+                                long long n, int* nf) {
   const long long tot = (long long)n_vec * n;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
     const long long v = e / n, j = e % n;
-    F[v * ldf + j] += Fn[v * ldn + j];
+    const double s = F[v * ldf + j] + Fn[v * ldn + j];
+    F[v * ldf + j] = s;
+    if (!isfinite(s)) *nf = 1;
   }
 }
 
 cudaError_t launch_add_rows(double* F, long long ldf, const double* Fn, long long ldn, int n_vec, long long n,
-                            cudaStream_t st) {
+                            int* nf, cudaStream_t st) {
   const long long tot = (long long)n_vec * n;
   long long b = (tot + 255) / 256;
   if (b > 148 * 32) b = 148 * 32;
   if (b < 1) return cudaSuccess;
-  note_launch(), add_rows_kernel<<<(unsigned)b, 256, 0, st>>>(F, ldf, Fn, ldn, n_vec, n);
+  note_launch(), add_rows_kernel<<<(unsigned)b, 256, 0, st>>>(F, ldf, Fn, ldn, n_vec, n, nf);
   return cudaGetLastError();
 }
 
 // Sum column-chunk partials of one row tile in chunk order.
 __global__ void near_reduce_kernel(const NearRowTile* rt, const double* part, double* F,
-                                   long long ldf, int n_vec, int overwrite) {
+                                   long long ldf, int n_vec, int overwrite, int* nf) {
   const NearRowTile t = rt[blockIdx.x];
   for (int e = threadIdx.x; e < kRT * n_vec; e += blockDim.x) {
     const int i = e % kRT, v = e / kRT;
@@ -272,7 +276,9 @@ __global__ void near_reduce_kernel(const NearRowTile* rt, const double* part, do
     for (int c = 0; c < t.nchunks; ++c)
       s += part[(t.part + c) * (long long)n_vec * kRT + (long long)v * kRT + i];
     double* dst = F + (long long)v * ldf + t.j0 + i;
-    *dst = overwrite ? s : *dst + s;
+    s = overwrite ? s : *dst + s;
+    *dst = s;
+    if (!isfinite(s)) *nf = 1;
   }
 }
 
@@ -303,9 +309,9 @@ cudaError_t launch_near(const NearArgs& a, int n_tiles, int n_groups, int max_co
 }
 
 cudaError_t launch_near_reduce(const NearRowTile* rt, int n_rt, const double* part, double* F,
-                               long long ldf, int n_vec, int overwrite, cudaStream_t st) {
+                               long long ldf, int n_vec, int overwrite, int* nf, cudaStream_t st) {
   if (n_rt == 0) return cudaSuccess;
-  note_launch(), near_reduce_kernel<<<n_rt, 256, 0, st>>>(rt, part, F, ldf, n_vec, overwrite);
+  note_launch(), near_reduce_kernel<<<n_rt, 256, 0, st>>>(rt, part, F, ldf, n_vec, overwrite, nf);
   return cudaGetLastError();
 }
 

@@ -195,3 +195,22 @@ def test_bench_csv(capsys, cuda_dev):
     rows = capsys.readouterr().out.strip().splitlines()
     assert rows[1].startswith("64,fast,") and rows[1].endswith(",")   # direct skipped: no error column
     assert rows[2].startswith("64,self-inverse,")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,n", [("schlomilch", 300), ("schlomilch", 40), ("dht", 200)])
+def test_transform_non_finite_output_exit_3(tmp_path, cuda_dev, capsys, kind, n):
+    """Reference cli.py:128-130: a non-finite output value is exit code 3 and
+    no output file.  Here the flag is raised on the device by the reductions
+    that write the output (fhtb_nonfinite_check -> FHTB_ENONFINITE)."""
+    c = np.random.default_rng([5, n]).standard_normal(n)
+    c[n // 2] = np.inf
+    src, dst = tmp_path / "c.bin", tmp_path / "f.bin"
+    fh.write_vector(str(src), c, "binary")
+    assert cli.main(["transform", kind, str(src), str(dst), "--format", "binary"]) == 3
+    assert "non-finite" in capsys.readouterr().err
+    assert not dst.exists()
+    # the flag is cleared by the check: a clean vector afterwards is exit 0
+    c[n // 2] = 1.0
+    fh.write_vector(str(src), c, "binary")
+    assert cli.main(["transform", kind, str(src), str(dst), "--format", "binary"]) == 0
