@@ -20,7 +20,7 @@ BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libfhtb200.so")
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 
-SOURCES = ["fhtb_host.cu", "fhtb_near.cu", "fhtb_far.cu", "fhtb_chirp.cu", "fhtb_misc.cu"]
+SOURCES = ["fhtb_host.cu", "fhtb_near.cu", "fhtb_far.cu", "fhtb_rowsum.cu", "fhtb_chirp.cu", "fhtb_misc.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",

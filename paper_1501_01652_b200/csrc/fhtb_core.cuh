@@ -213,28 +213,37 @@ template <int S> __device__ __forceinline__ double2 twid(const double2* __restri
 #ifndef FHTB_TW_COMPUTE
 #define FHTB_TW_COMPUTE 1
 #endif
-template <int R, int S>
-__device__ __forceinline__ void butterfly_twiddles(const double2* __restrict__ tw, int m, double2 (&w)[R]) {
+// tw is the size-N table inside the twiddle pool (pool + N - 2; the pool holds
+// the table of every power of two n at offset n - 2).  The butterflies of a
+// pass with span Ns need e^{S 2 pi i k r / n}, n = Ns R, k < Ns: w comes from
+// the size-n table, w^4 and w^8 from the size-n/4 and size-n/8 tables, all
+// indexed by k itself (same bits as tw[k N/n], tw[4 k N/n], tw[8 k N/n]), so
+// that a warp's gather touches consecutive entries instead of entries N/n,
+// 4 N/n and 8 N/n apart (up to 32 cache lines per request in the last pass).
+template <int N, int R, int S>
+__device__ __forceinline__ void butterfly_twiddles(const double2* __restrict__ tw, int n, int k, double2 (&w)[R]) {
   w[0] = make_double2(1.0, 0.0);
   if (R == 1) return;
   if (!FHTB_TW_COMPUTE) {
+    const int m = k * (N / n);
 #pragma unroll
     for (int r = 1; r < R; ++r) w[r] = twid<S>(tw, r * m);
     return;
   }
-  w[1] = twid<S>(tw, m);
+  const double2* pool = tw - (N - 2);
+  w[1] = twid<S>(pool + (n - 2), k);
   if (R >= 4) {
     w[2] = cmul(w[1], w[1]);
     w[3] = cmul(w[2], w[1]);
   }
   if (R >= 8) {
-    w[4] = twid<S>(tw, 4 * m);
+    w[4] = twid<S>(pool + (n / 4 - 2), k);
     w[5] = cmul(w[4], w[1]);
     w[6] = cmul(w[4], w[2]);
     w[7] = cmul(w[4], w[3]);
   }
   if (R >= 16) {
-    w[8] = twid<S>(tw, 8 * m);
+    w[8] = twid<S>(pool + (n / 8 - 2), k);
 #pragma unroll
     for (int r = 9; r < 12; ++r) w[r] = cmul(w[8], w[r - 8]);
     w[12] = cmul(w[8], w[4]);
@@ -257,13 +266,12 @@ __device__ __forceinline__ void stockham_mid(double2 (&v)[E], double2* sm, int t
 #pragma unroll
     for (int r = 0; r < R; ++r) v[b * R + r] = sm[swz<LOGE>(j + r * STR)];
   }
-  const int tstep = N / (Ns * R);
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     const int j = t + T * b;
     const int k = j % Ns;
     double2 w[R];
-    butterfly_twiddles<R, S>(tw, k * tstep, w);
+    butterfly_twiddles<N, R, S>(tw, Ns * R, k, w);
 #pragma unroll
     for (int r = 1; r < R; ++r) v[b * R + r] = cmul(v[b * R + r], w[r]);
     Dft<R, S>::run(v + b * R);

@@ -32,50 +32,9 @@
 
 #include "fhtb_core.cuh"
 #include "fhtb_launch.h"
+#include "fhtb_far.cuh"
 
 namespace fhtb {
-
-// x^p by binary powering (pre/post multipliers reach p = 10 per element)
-__device__ __forceinline__ double ipow_f(double x, int p) {
-  double r = 1.0;
-  for (; p; p >>= 1) {
-    if (p & 1) r *= x;
-    x *= x;
-  }
-  return r;
-}
-
-// Four-step twiddle e^{+2 pi i m / Q}.
-__device__ __forceinline__ double2 qtw(const FarArgs& a, long long m) {
-  const int lo = (int)(m & ((1LL << a.qbits) - 1));
-  const long long hi = m >> a.qbits;
-  double2 w = __ldg(a.qlo + lo);
-  if (hi) w = cmul(w, __ldg(a.qhi + hi));
-  return w;
-}
-
-// Column state of grid column n for request R on block B:
-//   v = x_n * omega_n^{-1/2},  iw = 1/omega_n   (0 outside the block)
-__device__ __forceinline__ void load_col(const FarArgs& a, const ReqDesc& R, long long cA, long long cB,
-                                         long long n, double& v, double& iw) {
-  v = 0.0;
-  iw = 0.0;
-  if (n >= cA && n < cB) {
-    double x = a.C[(long long)R.vec * a.ldc + (n - 1)];
-    if (R.preA) x *= ipow_f(R.preA[n - 1], R.pa);
-    if (R.preB) x *= ipow_f(R.preB[n - 1], R.pb);
-    // (computing beats loading w0_tab/iw_tab here: pass 1 28.1 vs 29.6 ms, cfg2)
-    const double om = ((double)n + a.gamma) * 3.141592653589793;
-    iw = 1.0 / om;
-    v = x * (1.0 / sqrt(om));
-  }
-}
-
-__device__ __forceinline__ void unit_cols(const FarArgs& a, const ReqDesc& R, const BlockDesc& B,
-                                          long long& cA, long long& cB) {
-  cA = max(max(B.c0, R.col_lo), 1LL);
-  cB = min(B.c1, min(a.n_data_cols + 1, a.L + 1));
-}
 
 // ------------------------------------------------------------------ pass 1
 // TMA: the twiddled outputs of the CTA's W columns are staged in shared
@@ -99,6 +58,7 @@ far_pass1_kernel(FarArgs a, const __grid_constant__ CUtensorMap gmap) {
   const UnitDesc U = a.units[a.u0 + ul];
   const ReqDesc& R = a.reqs[U.req];
   const BlockDesc& B = a.blocks[U.block];
+  const double bsig = B.sig, bisig = B.isig;
   long long cA, cB;
   unit_cols(a, R, B, cA, cB);
   // n = n1 + L1 n2 <= L  <=>  n2 < L2/2, or n2 = L2/2 with n1 = 0 (n = L):
@@ -130,12 +90,12 @@ far_pass1_kernel(FarArgs a, const __grid_constant__ CUtensorMap gmap) {
 #pragma unroll
     for (int e = 0; e < EH; ++e) {
       const double im = v[e] * iw[e];
-      z[e] = make_double2(v[e], im);
+      z[e] = make_double2(v[e], im * bsig);
       v[e] = im * iw[e];
       z[e + EH] = make_double2(0.0, 0.0);
     }
     const double ims = vs * iws;
-    const double2 extra = make_double2(vs, ims);
+    const double2 extra = make_double2(vs, ims * bsig);
     vs = ims * iws;
     if (TMA) {
       // the previous pair's tensor store may still read the staging area:
@@ -206,6 +166,7 @@ far_pass1p_kernel(FarArgs a) {
   const UnitDesc U = a.units[a.u0 + ul];
   const ReqDesc& R = a.reqs[U.req];
   const BlockDesc& B = a.blocks[U.block];
+  const double bsig = B.sig, bisig = B.isig;
   long long cA, cB;
   unit_cols(a, R, B, cA, cB);
   double2 z[E];
@@ -225,7 +186,7 @@ far_pass1p_kernel(FarArgs a) {
         if (q & 1) v *= b2;
         b2 *= b2;
       }
-      z[e] = make_double2(v, v * iw);
+      z[e] = make_double2(v, (v * iw) * bsig);
     }
   }
   double2* sm = sm2 + w * NP;
@@ -286,6 +247,7 @@ far_pass2_kernel(FarArgs a) {
   const UnitDesc U = a.units[a.u0 + ul];
   const ReqDesc& R = a.reqs[U.req];
   const BlockDesc& B = a.blocks[U.block];
+  const double bsig = B.sig, bisig = B.isig;
   const double2* tw = a.tw + (N1 - 2);
   const int xj = XCH ? __ldg(a.xrow + myk2).y : 0;
   // L2 = Q / N1 is a power of two: k / L2 as a shift (a runtime division
@@ -376,7 +338,7 @@ far_pass2_kernel(FarArgs a) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const double im = v[ONEPASS ? e : 0] * iw[ONEPASS ? e : 0];
-        z[e] = make_double2(v[ONEPASS ? e : 0], im);
+        z[e] = make_double2(v[ONEPASS ? e : 0], im * bsig);
         v[ONEPASS ? e : 0] = im * iw[ONEPASS ? e : 0];
       }
     } else if (MODE == 2) {
@@ -410,7 +372,7 @@ far_pass2_kernel(FarArgs a) {
     double ac0, bc0, ac1, bc1;
     if (E <= 8) {
       ac0 = R.ac[i0], bc0 = R.bc[i0];
-      ac1 = R.ac[i1], bc1 = R.bc[i1];
+      ac1 = R.ac[i1] * bisig, bc1 = R.bc[i1] * bisig;
     }
     __syncthreads();
     block_fft<N1, E, 1>(z, sm2 + h * NP, tt, tw);
@@ -420,7 +382,7 @@ far_pass2_kernel(FarArgs a) {
     __syncthreads();
     if (E > 8) {
       ac0 = R.ac[i0], bc0 = R.bc[i0];
-      ac1 = R.ac[i1], bc1 = R.bc[i1];
+      ac1 = R.ac[i1] * bisig, bc1 = R.bc[i1] * bisig;
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -495,6 +457,7 @@ __global__ void colgen_prep_kernel(FarArgs a) {
   const UnitDesc U = a.units[a.u0 + ul];
   const ReqDesc& R = a.reqs[U.req];
   const BlockDesc& B = a.blocks[U.block];
+  const double bsig = B.sig, bisig = B.isig;
   long long cA, cB;
   unit_cols(a, R, B, cA, cB);
   const long long n = m + cA;
@@ -503,7 +466,7 @@ __global__ void colgen_prep_kernel(FarArgs a) {
   double2* u = a.G + (long long)(ul * a.M) * a.L1 + m;
   for (int p = 0; p < a.M; ++p) {
     const double im = v * iw;
-    u[(long long)p * a.L1] = make_double2(v, im);
+    u[(long long)p * a.L1] = make_double2(v, im * bsig);
     v = im * iw;
   }
 }
@@ -534,6 +497,7 @@ far_rowdot_kernel(FarArgs a, int c_lo) {
   const UnitDesc U = a.units[a.u0 + ul];
   const ReqDesc& R = a.reqs[U.req];
   const BlockDesc& B = a.blocks[U.block];
+  const double bsig = B.sig, bisig = B.isig;
   // all KB bins are summed (compile-time trip counts keep the loads of the
   // unrolled n1 loop in flight together); bins past the block rows are not
   // written
@@ -611,7 +575,7 @@ far_rowdot_kernel(FarArgs a, int c_lo) {
     double2 Yb = make_double2(Zk.y - Zp.y, Zp.x - Zk.x);
     if (k == L) { Ya.y = 0.0; Yb.y = 0.0; }
     const int i0 = 2 * p, i1 = 2 * p + 1;
-    const double ac0 = R.ac[i0], bc0 = R.bc[i0], ac1 = R.ac[i1], bc1 = R.bc[i1];
+    const double ac0 = R.ac[i0], bc0 = R.bc[i0], ac1 = R.ac[i1] * bisig, bc1 = R.bc[i1] * bisig;
     const double t0x = fma(ac0, Ya.x, bc0 * Ya.y), t0y = fma(ac0, Ya.y, -bc0 * Ya.x);
     const double t1x = fma(ac1, Yb.x, bc1 * Yb.y), t1y = fma(ac1, Yb.y, -bc1 * Yb.x);
     const double w2 = ir * ir;
@@ -643,6 +607,7 @@ far_rowdot1_kernel(FarArgs a, int c_lo) {
   const UnitDesc U = a.units[a.u0 + ul];
   const ReqDesc& R = a.reqs[U.req];
   const BlockDesc& B = a.blocks[U.block];
+  const double bsig = B.sig, bisig = B.isig;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int cb = (L2 - c) % L2;
   // outputs: k = c (needs Z[c] = S0(c), conj Z[2L-c] = conj S1(cb)) and
@@ -701,7 +666,7 @@ far_rowdot1_kernel(FarArgs a, int c_lo) {
     double2 Yb = make_double2(Zk.y - Zp.y, Zp.x - Zk.x);
     if (k == L) { Ya.y = 0.0; Yb.y = 0.0; }
     const int i0 = 2 * p, i1 = 2 * p + 1;
-    const double ac0 = R.ac[i0], bc0 = R.bc[i0], ac1 = R.ac[i1], bc1 = R.bc[i1];
+    const double ac0 = R.ac[i0], bc0 = R.bc[i0], ac1 = R.ac[i1] * bisig, bc1 = R.bc[i1] * bisig;
     const double t0x = fma(ac0, Ya.x, bc0 * Ya.y), t0y = fma(ac0, Ya.y, -bc0 * Ya.x);
     const double t1x = fma(ac1, Yb.x, bc1 * Yb.y), t1y = fma(ac1, Yb.y, -bc1 * Yb.x);
     const double w2 = ir * ir;
@@ -717,194 +682,6 @@ far_rowdot1_kernel(FarArgs a, int c_lo) {
   if (a.cs_tab) {
     const double2 th = __ldg(a.cs_tab + (k - 1));
     v = v * th.x + (acc.y * r0) * th.y;
-  }
-  a.part[(long long)ul * a.part_stride + (k - 1)] = v;
-}
-
-// ------------------------------------------- narrow rows, fully fused form
-//
-// A block whose rows all lie below L2 = 2^lr (lr <= 12) needs, per column n1,
-// only the bin k1 = 0 of pass 2 and its partner:
-//     Z_p[k]          = S0_p[k]      = sum_n1 t(n1, k)      F_{p,n1}[k]
-//     conj Z_p[2L-k]  = conj S1_p[k'] , S1_p[k'] = sum_n1 t(n1, k' - L2) F_{p,n1}[k'],  k' = L2 - k
-// with F_{p,n1} the L2-point column FFT of pair p and t(n1, m) = e^{2 pi i n1 m / Q}.
-// The row epilogue is linear in Z_p[k] and antilinear in Z_p[2L-k]:
-//     U_k = sum_p (L/k)^{2p} [ alpha_p(k) S0_p[k] + beta_p(k) conj S1_p[L2-k] ],
-//     alpha_p = c0_p - i (L/k) c1_p,  beta_p = c0_p + i (L/k) c1_p,  c_i = a_i - i b_i,
-// so the sum over the pairs is folded PER COLUMN, in the registers of the
-// thread that holds FFT output k2, before the sum over the columns:
-//     A_n1[k2] = sum_p (L/k)^{2p} alpha_p(k) F_{p,n1}[k2]            (k = k2      in the block rows)
-//     B_n1[k2] = sum_p (L/k)^{2p} conj(beta_p(k)) F_{p,n1}[k2]       (k = L2 - k2 in the block rows)
-//     U_k = sum_n1 t(n1, k) A_n1[k]  +  conj( sum_n1 t(n1, -k) B_n1[L2-k] ).
-// One CTA = W columns of one unit (as pass 1): the coefficients are loaded
-// once, the M column FFTs run back to back with Horner's rule over the pairs
-// from the last one down, and only the folded values of the block's rows
-// leave the CTA: P[unit][A|B][row][n1] (2 * rows * L1 complex per unit
-// instead of M * 2L, no pass 2, no row sums over the intermediate).
-// far_rowsum_fin_kernel sums P over n1 in a fixed order and finishes the row.
-//
-// The pairs run downwards, so the column state goes from pair p to p-1 by one
-// multiplication with omega_n^2; its start omega_n^{-2(p1-1)-1/2} x_n is built
-// by the same multiplication sequence as pass 1.
-// A k2 that serves both a row k2 and a row L2 - k2 (L2 - r1 < k2 < r1) keeps
-// its second accumulator in shared memory (thread-private slot).
-template <int N2, int W, int MINB>
-__global__ void __launch_bounds__(W * (N2 / 16), MINB)
-far_rowsum_kernel(FarArgs a) {
-  constexpr int E = 16, T = N2 / E, EH = E / 2, NTH = W * T;
-  constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
-  constexpr int NP = N2 + PAD;
-  extern __shared__ __align__(16) double2 sm2[];
-  double* wA = reinterpret_cast<double*>(sm2 + W * NP);     // [s][tid]: L/k, k = k2
-  double* wB = wA + E * NTH;                                // [s][tid]: L/k, k = N2 - k2
-  double2* A2 = reinterpret_cast<double2*>(wB + E * NTH);   // [s][tid]: B where A and B share a k2
-  const int tid = threadIdx.x, w = tid % W, tt = tid / W;
-  const int L1 = a.L1;
-  const long long n1 = (long long)blockIdx.x * W + w;
-  const int ul = blockIdx.y;
-  const UnitDesc U = a.units[a.u0 + ul];
-  const ReqDesc& R = a.reqs[U.req];
-  const BlockDesc& B = a.blocks[U.block];
-  long long cA, cB;
-  unit_cols(a, R, B, cA, cB);
-  const int R0 = (int)max(B.r0, 1LL), R1 = (int)min(B.r1, (long long)N2);
-  unsigned m0 = 0, m1 = 0;
-#pragma unroll
-  for (int s = 0; s < E; ++s) {
-    const int k2 = fft_out_index<N2, E>(tt, s), kb = N2 - k2;
-    const bool t0 = k2 >= R0 && k2 < R1, t1 = k2 >= 1 && kb >= R0 && kb < R1;
-    m0 |= (unsigned)t0 << s;
-    m1 |= (unsigned)t1 << s;
-    wA[s * NTH + tid] = t0 ? a.Ld / (double)k2 : 0.0;
-    wB[s * NTH + tid] = t1 ? a.Ld / (double)kb : 0.0;
-    A2[s * NTH + tid] = make_double2(0.0, 0.0);
-  }
-  // column state at the shard's last pair
-  double u[EH], iw[EH], om2[EH], us = 0.0, iws = 0.0, om2s = 0.0;
-#pragma unroll
-  for (int e = 0; e < EH; ++e) {
-    const long long n = n1 + (long long)L1 * (tt + T * e);
-    load_col(a, R, cA, cB, n, u[e], iw[e]);
-    const double om = ((double)n + a.gamma) * 3.141592653589793;
-    om2[e] = om * om;
-  }
-  if (tt == 0 && n1 == 0) {
-    const long long n = (long long)L1 * (T * EH);
-    load_col(a, R, cA, cB, n, us, iws);
-    const double om = ((double)n + a.gamma) * 3.141592653589793;
-    om2s = om * om;
-  }
-  for (int p = 0; p < a.p1 - 1; ++p) {
-#pragma unroll
-    for (int e = 0; e < EH; ++e) u[e] = (u[e] * iw[e]) * iw[e];
-    us = (us * iws) * iws;
-  }
-  double2 A[E];
-#pragma unroll
-  for (int s = 0; s < E; ++s) A[s] = make_double2(0.0, 0.0);
-  const double2* tw = a.tw + (N2 - 2);
-  double2* sm = sm2 + w * NP;
-  for (int p = a.p1 - 1; p >= a.p0; --p) {
-    double2 z[E];
-#pragma unroll
-    for (int e = 0; e < EH; ++e) {
-      z[e] = make_double2(u[e], u[e] * iw[e]);
-      z[e + EH] = make_double2(0.0, 0.0);
-      u[e] *= om2[e];
-    }
-    const double2 extra = make_double2(us, us * iws);
-    us *= om2s;
-    // (the barrier after the register-only first radix pass separates the
-    // previous pair's last shared-memory reads from this pair's writes)
-    block_fft<N2, E, 1, true, true>(z, sm, tt, tw, extra);
-    const double c0x = R.ac[2 * p], c0y = -R.bc[2 * p];
-    const double c1x = R.ac[2 * p + 1], c1y = -R.bc[2 * p + 1];
-#pragma unroll
-    for (int s = 0; s < E; ++s) {
-      const bool t0 = (m0 >> s) & 1u, t1 = (m1 >> s) & 1u;
-      if (t0 || t1) {
-        // alpha = c0 - i wk c1 (row k2), or conj(beta) = conj(c0) - i wk conj(c1) (row N2 - k2)
-        const double wk = t0 ? wA[s * NTH + tid] : wB[s * NTH + tid];
-        const double gx = t0 ? fma(wk, c1y, c0x) : fma(-wk, c1y, c0x);
-        const double gy = t0 ? fma(-wk, c1x, c0y) : fma(-wk, c1x, -c0y);
-        const double w2 = wk * wk;
-        A[s].x = fma(A[s].x, w2, fma(gx, z[s].x, -gy * z[s].y));
-        A[s].y = fma(A[s].y, w2, fma(gx, z[s].y, gy * z[s].x));
-      }
-      if (t0 && t1) {
-        const double wk = wB[s * NTH + tid];
-        const double gx = fma(-wk, c1y, c0x), gy = fma(-wk, c1x, -c0y), w2 = wk * wk;
-        double2 t = A2[s * NTH + tid];
-        t.x = fma(t.x, w2, fma(gx, z[s].x, -gy * z[s].y));
-        t.y = fma(t.y, w2, fma(gx, z[s].y, gy * z[s].x));
-        A2[s * NTH + tid] = t;
-      }
-    }
-  }
-  // four-step twiddles, once per column, and the folded rows out
-  const long long qm = (1LL << a.logQ) - 1;
-  double2* P0 = a.G + ((long long)(2 * ul) * a.rs) * L1 + n1;
-  double2* P1 = a.G + ((long long)(2 * ul + 1) * a.rs) * L1 + n1;
-#pragma unroll
-  for (int s = 0; s < E; ++s) {
-    const bool t0 = (m0 >> s) & 1u, t1 = (m1 >> s) & 1u;
-    const int k2 = fft_out_index<N2, E>(tt, s), kb = N2 - k2;
-    if (t0) P0[(long long)(k2 - R0) * L1] = cmul(A[s], qtw(a, (n1 * k2) & qm));
-    if (t1) {
-      const double2 b = t0 ? A2[s * NTH + tid] : A[s];
-      P1[(long long)(kb - R0) * L1] = cmul(b, qtw(a, (n1 * (long long)(k2 - N2)) & qm));
-    }
-  }
-}
-
-// U_k = sum_n1 P[A][row][n1] + conj(sum_n1 P[B][row][n1]), the row scale
-// (1/2) post_k (L/k)^{1/2 + 2 p0} and the gamma rotation; one CTA per
-// (row, unit), n1 summed by strided threads and a fixed-order tree.
-__global__ void __launch_bounds__(128)
-far_rowsum_fin_kernel(FarArgs a) {
-  const int ul = blockIdx.y;
-  const UnitDesc U = a.units[a.u0 + ul];
-  const ReqDesc& R = a.reqs[U.req];
-  const BlockDesc& B = a.blocks[U.block];
-  const int R0 = (int)max(B.r0, 1LL), R1 = (int)min(B.r1, (long long)a.L2);
-  const int k = R0 + (int)blockIdx.x;
-  if (k >= R1) return;
-  const int L1 = a.L1, tid = threadIdx.x;
-  const double2* P0 = a.G + ((long long)(2 * ul) * a.rs + blockIdx.x) * L1;
-  const double2* P1 = a.G + ((long long)(2 * ul + 1) * a.rs + blockIdx.x) * L1;
-  double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
-#pragma unroll 4
-  for (int n1 = tid; n1 < L1; n1 += 128) {
-    s0 = cadd(s0, P0[n1]);
-    s1 = cadd(s1, P1[n1]);
-  }
-#pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    s0.x += __shfl_xor_sync(0xffffffffu, s0.x, off);
-    s0.y += __shfl_xor_sync(0xffffffffu, s0.y, off);
-    s1.x += __shfl_xor_sync(0xffffffffu, s1.x, off);
-    s1.y += __shfl_xor_sync(0xffffffffu, s1.y, off);
-  }
-  __shared__ double2 red[4][2];
-  if ((tid & 31) == 0) {
-    red[tid >> 5][0] = s0;
-    red[tid >> 5][1] = s1;
-  }
-  __syncthreads();
-  if (tid) return;
-  s0 = cadd(cadd(red[0][0], red[1][0]), cadd(red[2][0], red[3][0]));
-  s1 = cadd(cadd(red[0][1], red[1][1]), cadd(red[2][1], red[3][1]));
-  const double ux = s0.x + s1.x, uy = s0.y - s1.y;
-  const double ir = a.Ld / (double)k;
-  double post = 1.0;
-  if (R.pr) post = ipow_f((double)k / a.Ld, R.pr);
-  if (R.post_e && R.pe) post *= ipow_f(R.post_e[k - 1], R.pe);
-  double r0 = 0.5 * post * sqrt(ir);
-  for (int p = 0; p < a.p0; ++p) r0 = (r0 * ir) * ir;           // (L/k)^{2 p0}
-  double v = ux * r0;
-  if (a.cs_tab) {
-    const double2 th = __ldg(a.cs_tab + (k - 1));
-    v = v * th.x + (uy * r0) * th.y;
   }
   a.part[(long long)ul * a.part_stride + (k - 1)] = v;
 }
@@ -939,6 +716,7 @@ far_pass2x_kernel(FarArgs a) {
   const UnitDesc U = a.units[a.u0 + ul];
   const ReqDesc& R = a.reqs[U.req];
   const BlockDesc& B = a.blocks[U.block];
+  const double bsig = B.sig, bisig = B.isig;
   const double2* tw = a.tw + (N1 - 2);
 
   // computing slots: e' = slot index in "t + T e'" order; half 0 owns
@@ -1003,7 +781,7 @@ far_pass2x_kernel(FarArgs a) {
     }
     const int i0 = 2 * p, i1 = 2 * p + 1;
     const double ac0 = R.ac[i0], as0 = R.as[i0], bc0 = R.bc[i0], bs0 = R.bs[i0];
-    const double ac1 = R.ac[i1], as1 = R.as[i1], bc1 = R.bc[i1], bs1 = R.bs[i1];
+    const double ac1 = R.ac[i1] * bisig, as1 = R.as[i1] * bisig, bc1 = R.bc[i1] * bisig, bs1 = R.bs[i1] * bisig;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int k = kq[q];
@@ -1242,37 +1020,6 @@ cudaError_t launch_prefetch_rows(const FarArgs& a, int n_units, cudaStream_t st)
   const long long lines = (a.n_data_cols * 8 + 127) / 128;
   const int bx = (int)std::min<long long>((lines + 255) / 256, 64);
   note_launch(), prefetch_rows_kernel<<<dim3(bx, n_units), 256, 0, st>>>(a);
-  return cudaGetLastError();
-}
-
-template <int N2, int W, int MINB>
-static cudaError_t rowsum_t(const FarArgs& a, int n_units, cudaStream_t st) {
-  constexpr int T = N2 / 16, NTH = W * T;
-  constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
-  const int smem = W * (N2 + PAD) * 16 + 16 * NTH * (8 + 8 + 16);   // FFT buffers + L/k tables + second accumulators
-  auto k = far_rowsum_kernel<N2, W, MINB>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  if (a.L1 % W) return cudaErrorInvalidValue;
-  note_launch(), k<<<dim3(a.L1 / W, n_units), NTH, smem, st>>>(a);
-  return cudaGetLastError();
-}
-
-// Fused narrow-row units: column FFTs of 2^logN2 points, folded rows to P (a.G).
-cudaError_t launch_far_rowsum(const FarArgs& a, int logN2, int n_units, cudaStream_t st) {
-  switch (logN2) {
-    case 7: return rowsum_t<128, 16, 2>(a, n_units, st);
-    case 8: return rowsum_t<256, 8, 2>(a, n_units, st);
-    case 9: return rowsum_t<512, 4, 2>(a, n_units, st);
-    case 10: return rowsum_t<1024, 2, 2>(a, n_units, st);
-    case 11: return rowsum_t<2048, 1, 2>(a, n_units, st);
-    case 12: return rowsum_t<4096, 1, 1>(a, n_units, st);
-  }
-  return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_far_rowsum_fin(const FarArgs& a, int n_units, cudaStream_t st) {
-  note_launch(), far_rowsum_fin_kernel<<<dim3(a.rs, n_units), 128, 0, st>>>(a);
   return cudaGetLastError();
 }
 

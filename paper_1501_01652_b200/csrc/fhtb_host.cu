@@ -38,7 +38,8 @@ int g_far_streams = 2;                     // far-field chunks in flight (direct
 int g_near_overlap = 1;                    // near field on its own stream beside the far field
 int g_serial = 0;                          // diagnostics: every launch on the caller's stream, in order
 int g_prune_rows = 11;                     // narrow-row blocks: rows below 2^g_prune_rows
-int g_rowsum = 1;                          // narrow-row blocks: fully fused form (dmode 3) where it applies
+int g_rowsum = 2;                          // narrow-row blocks: fully fused forms (dmode 3..5); 1: only blocks that would run both passes; 0: off
+int g_rowsum_min_m = 4;                    // ... for blocks already pruned to row sums: only with at least this many pairs
 int g_rowdot_bins = 1;                     // narrow-row blocks: at most this many pass-2 bins per column
 int g_min_lc = 9;                          // narrow-column blocks: smallest column FFT 2^g_min_lc
 int g_near_priority = 0;                   // near-field stream priority (see get_aux)
@@ -653,6 +654,10 @@ int fhtb_set_option(const char* key, int64_t value) {
     g_rowsum = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2));
     return FHTB_OK;
   }
+  if (!std::strcmp(key, "far_rowsum_min_pairs")) {
+    g_rowsum_min_m = (int)std::max<int64_t>(1, value);
+    return FHTB_OK;
+  }
   if (!std::strcmp(key, "far_rowdot_bins")) {
     if (value < 1 || value > 4) return fail(FHTB_EINVAL, "far_rowdot_bins must be 1..4");
     g_rowdot_bins = (int)value;
@@ -881,19 +886,40 @@ int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
         x.dmode = 2;                 // narrow rows with a longer pass-1 FFT, one bin
         x.dlogL1 = g->logQ - lr;
       }
-      // narrow rows, fully fused (far_rowsum_kernel): column FFTs of
-      // 2^ls >= r1 points (128..4096), pairs folded per column, no
-      // intermediate.  Needs r1 <= 2^ls < L and at least 16 columns n1.
-      const int ls = std::max(7, ilog2ll(std::max<long long>(x.r1, 2)));
-      // g_rowsum 1: only where the block would otherwise run the full pass 1 + pass 2
-      // (measured on cfg2: 17.3 vs 25.2 us per unit and pair at 4096 points; the
-      // 1024- and 128-point shapes lose to pass 1 + row sums, 14.7 / 26 vs 13.5 us);
-      // 2: every narrow-row block
-      if (g_far_prune && g_rowsum && (x.dmode == 0 || (x.dmode == 2 && g_rowsum >= 2)) && ls <= 12 &&
-          g->logQ - ls >= 4 && (1LL << ls) < g->L) {
-        x.dmode = 3;
-        x.dlogL1 = g->logQ - ls;
-        x.kbins = 1;
+      // narrow rows, fully fused (fhtb_rowsum.cu): column FFTs of 2^ls >= r1
+      // points (128..4096), pairs folded per column, no intermediate.  Needs
+      // r1 <= 2^ls < L and at least 16 columns n1.  dmode 3 + form:
+      //   form 1: high-occupancy kernel, no k2 serves two rows (2 r1 <= 2^ls + 1)
+      //   form 2: same with up to two such k2 per thread (2 r1 - 2^ls - 1 <= 2^ls / 16)
+      //   form 0: accumulators in registers, any overlap (2048 / 4096 points)
+      // g_rowsum 1: blocks that would otherwise run the full pass 1 + pass 2 use
+      // form 0 at 4096 points (cfg2: 17.3 vs 25.2 us per unit and pair) and the
+      // high-occupancy forms; 2: also the blocks already pruned to row sums.
+      const bool was_rows = x.dmode == 2;     // already pruned to pass 1 + row sums
+      if (g_far_prune && g_rowsum && (x.dmode == 0 || (was_rows && g_rowsum >= 2 && g->M >= g_rowsum_min_m))) {
+        int ls = std::max(7, ilog2ll(std::max<long long>(x.r1, 2)));
+        long long ov = 2 * x.r1 - (1LL << ls) - 1;          // k2 in (2^ls - r1, r1) serve two rows
+        int form = -1;
+        if (ls <= 11 && ov <= 0) form = 1;
+        else if (ls <= 11 && ov <= (1LL << ls) / 16) form = 2;
+        else if (ls + 1 <= 11) { ls += 1; form = 1; }
+        else if (ls <= 12 && !was_rows) form = 0;
+        if (form >= 0 && g->logQ - ls >= 4 && (1LL << ls) < g->L) {
+          x.dmode = 3 + form;
+          x.dlogL1 = g->logQ - ls;
+          x.kbins = 1;
+        }
+      }
+    }
+    x.sig = x.isig = 1.0;
+    if (g->direct) {
+      // exact power of two near omega at the block's first column (fhtb_types.h)
+      const double om0 = ((double)std::max<long long>(x.c0, 1) + g->gamma) * M_PI;
+      if (om0 > 1.0) {
+        int ex = 0;
+        std::frexp(om0, &ex);
+        x.sig = std::ldexp(1.0, ex - 1);
+        x.isig = 1.0 / x.sig;
       }
     }
     g->bdesc.push_back(x);
@@ -952,7 +978,7 @@ double fhtb_grid_far_model_bytes(const fhtb_grid* g) {
     } else if (x.dmode == 2) {
       const double L2 = (double)(1LL << (g->logQ - x.dlogL1));
       bytes += terms * 16.0 * L * (1.0 + std::min(1.0, 2.0 * (rows + 1) / L2));
-    } else if (x.dmode == 3) {
+    } else if (x.dmode >= 3) {
       bytes += 2.0 * 32.0 * rows * (double)(1LL << x.dlogL1);   // folded rows P written and read
     }                                                       // dmode 1: no intermediate
   }
@@ -1046,7 +1072,7 @@ void plan_far(const fhtb_grid* g, const std::vector<ReqDesc>& rs, FarPlan& fp, i
       // narrow-column units keep only their column table (M x L1)
       size_t ub = (key / 64 == 1) ? (size_t)g->M * ((size_t)1 << (key % 64)) * sizeof(double2)
                                   : unit_bytes_q(g, g->logQ);
-      if (key / 64 == 3) {
+      if (key / 64 >= 3) {
         // fused narrow rows: P[unit][A|B][rows][L1], rows = the widest block of the group
         long long rs = 1;
         for (size_t i = 0; i < all.size(); ++i)
@@ -1543,7 +1569,7 @@ void chunk_bytes(const fhtb_grid* g, const FarPlan& fp, size_t ci, const std::ve
       const double l1 = (double)(1LL << x.dlogL1);
       out[0] += 8.0 * cols + np * 16.0 * l1;                          // column table written
       out[1] += np * 16.0 * l1 + 8.0 * rows;                          // read, partial row
-    } else if (x.dmode == 3) {
+    } else if (x.dmode >= 3) {
       const double l1 = (double)(1LL << x.dlogL1);
       out[0] += 8.0 * cols + 32.0 * rows * l1;                        // folded rows written
       out[1] += 32.0 * rows * l1 + 8.0 * rows;                        // read, partial row
@@ -1792,12 +1818,12 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
             if (mode != 1 && g_far_prefetch) KT(kfOther, cs, 0.0, launch_prefetch_rows(a, n_units, cs));
             if (mode == 1) {
               KT(kfNarrow, cs, cb[0] + cb[1], launch_far_colgen(a, l1, n_units, cs));
-            } else if (mode == 3) {
+            } else if (mode >= 3) {
               long long rs = 1;
               for (int u = fp.chunks[ci].x; u < fp.chunks[ci].y; ++u)
                 rs = std::max(rs, fused_rows(g, g->bdesc[fp.units[u].block], l1));
               a.rs = (int)rs;
-              KT(kfRowsum, cs, cb[0], launch_far_rowsum(a, l2, n_units, cs));
+              KT(kfRowsum, cs, cb[0], launch_far_rowsum(a, l2, mode - 3, n_units, cs));
               KT(kfRowsumFin, cs, cb[1], launch_far_rowsum_fin(a, n_units, cs));
             } else if (mode == 2) {
               KT(kfPass1, cs, cb[0], launch_far_pass1(a, l2, n_units, cs));

@@ -108,7 +108,7 @@ cudaError_t launch_far_pass2x_range(const FarArgs& a, int logN1, int n_pairs, in
 cudaError_t launch_far_reduce(const FarArgs& a, int n_units, cudaStream_t st);
 cudaError_t launch_far_colgen(const FarArgs& a, int logN1, int n_units, cudaStream_t st);
 cudaError_t launch_far_rowdot(const FarArgs& a, int n_units, int kbins, cudaStream_t st);
-cudaError_t launch_far_rowsum(const FarArgs& a, int logN2, int n_units, cudaStream_t st);
+cudaError_t launch_far_rowsum(const FarArgs& a, int logN2, int form, int n_units, cudaStream_t st);
 cudaError_t launch_far_rowsum_fin(const FarArgs& a, int n_units, cudaStream_t st);
 cudaError_t launch_prefetch_rows(const FarArgs& a, int n_units, cudaStream_t st);
 cudaError_t launch_cs_table(double2* cs, long long L, double gamma, double pi_over_L, cudaStream_t st);

@@ -45,6 +45,13 @@ struct BlockDesc {
   int dlogL1;
   // dmode 2: FFT bins k1 < kbins of each column are needed (rows k < kbins * L2)
   int kbins;
+  // direct mode: terms 2p (real part) and 2p+1 (imaginary part) share one
+  // complex FFT; u_{2p+1} = u_{2p} / omega_n is smaller by omega_n, and what the
+  // separation Z[k] -/+ conj Z[2L-k] loses is amplified by the row factor L/k
+  // (1e-10 relative at N = 2^24, k ~ 10).  The imaginary part is therefore
+  // carried times sig = 2^floor(log2 omega_{c0}) (exact) and the odd-term
+  // coefficients times isig = 1/sig.
+  double sig, isig;
   int pad2_;
 };
 

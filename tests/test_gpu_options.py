@@ -19,7 +19,7 @@ from paper_1501_01652_b200.schlomilch import _grid_cache, _grid_lock
 pytestmark = pytest.mark.gpu
 
 DEFAULTS = {b"far_rowdot_bins": 1, b"far_min_cols": 9, b"near_chunk_cols": 8192,
-            b"near_chunk_cols_multi": 1024, b"far_prefetch": 1, b"near_priority": 0, b"far_prune_rows": 11}
+            b"near_chunk_cols_multi": 1024, b"far_prefetch": 1, b"near_priority": 0, b"far_prune_rows": 11, b"far_rowsum": 2}
 
 
 def _set(opts):
@@ -47,7 +47,12 @@ def _schl(n, nu, gamma, eps, batch, seed):
 # past 1024 (rows up to 1760 at 2^19: two bins; 2488 at 2^20: three); the
 # others already act at 2^17
 @pytest.mark.parametrize("opts,n", [
-    ({b"far_rowdot_bins": 2}, 2 ** 19), ({b"far_rowdot_bins": 4}, 2 ** 20), ({b"far_prune_rows": 12}, 2 ** 20),
+    # the narrow-row forms: fused (default, far_rowsum 2), fused only for blocks that
+    # would run the full two passes (1), pass 1 + row sums / full two passes (0)
+    ({b"far_rowsum": 0}, 2 ** 20), ({b"far_rowsum": 1}, 2 ** 20), ({b"far_rowsum": 0}, 2 ** 17),
+    ({b"far_rowsum": 0}, 2 ** 15), ({b"far_rowsum": 0}, 2 ** 22),
+    ({b"far_rowsum": 0, b"far_rowdot_bins": 2}, 2 ** 19), ({b"far_rowsum": 0, b"far_rowdot_bins": 4}, 2 ** 20),
+    ({b"far_rowsum": 0, b"far_prune_rows": 12}, 2 ** 20),
     ({b"far_min_cols": 7}, 2 ** 17), ({b"far_min_cols": 12}, 2 ** 17), ({b"far_prefetch": 0}, 2 ** 17),
     ({b"near_chunk_cols": 512}, 2 ** 17),
 ])
@@ -75,9 +80,9 @@ def test_rowdot_bins_cover_wide_row_blocks(cuda_dev, restore):
     n, nu, gamma, eps = 2 ** 20, 4, 4.0, 1e-15
     c, p = _schl(n, nu, gamma, eps, 2, 13)
     sc = fh.build_partition(p)
-    _set(DEFAULTS)
+    _set({**DEFAULTS, b"far_rowsum": 0})
     ref = fh.schlomilch_fast(p, c)
-    _set({**DEFAULTS, b"far_rowdot_bins": 4})
+    _set({**DEFAULTS, b"far_rowsum": 0, b"far_rowdot_bins": 4})
     got = fh.schlomilch_fast(p, c)
     (r0, r1), _ = sc.blocks[1]                  # rows [a_1, a_0): 539..2487 at cfg2
     assert r1 - 1 > 2 * 1024                    # needs more than two bins of L2 = 1024

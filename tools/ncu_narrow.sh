@@ -12,5 +12,8 @@ timeout 1500 ncu --set full --clock-control none --import-source on -k regex:$K 
 echo "ncu rc=$?"
 ncu -i /tmp/$TAG.ncu-rep --page details --csv > gpurun_out/${TAG}_details.csv
 ncu -i /tmp/$TAG.ncu-rep --page raw --csv > gpurun_out/${TAG}_raw.csv
-ncu -i /tmp/$TAG.ncu-rep --page source --csv --print-source cuda > gpurun_out/${TAG}_source.csv 2>/dev/null
+# hot source lines per captured kernel (stall samples / executed instructions per line)
+for kn in "far_pass2_kernel<2048, 16, 0" "far_pass2_kernel<512" "far_pass2_kernel<2048, 16, 2" "far_pass1" "far_rowsum_kernel" "far_rowsum2_kernel<256" "far_rowsum2_kernel<1024"; do
+  echo "== $kn"; python tools/ncu_lines.py /tmp/$TAG.ncu-rep "$kn" 45
+done > gpurun_out/${TAG}_lines.txt 2>&1
 ls -la /tmp/$TAG.ncu-rep gpurun_out/
