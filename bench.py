@@ -267,12 +267,17 @@ def kernel_roofline(kt, steps, peak, step_ms, kt_step=None, steps_step=1):
     (kernels then share the SMs, so those times overlap and sum past the step)."""
     out = []
     tot = sum(v["ms"] for v in kt.values()) / steps
+    f64 = (fp64_peaks() or {}).get("dfma_tflops")
     for name, v in sorted(kt.items(), key=lambda kv: -kv[1]["ms"]):
         ms = v["ms"] / steps
         gbs = v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] > 0 else 0.0
+        tfl = v.get("flops", 0.0) / (v["ms"] / 1e3) / 1e12 if v["ms"] > 0 else 0.0
         k = {"kernel": name, "ms_per_step": ms, "share_of_step": ms / tot if tot else None,
              "launches_per_step": v["launches"] / steps, "bytes_per_step": v["bytes"] / steps,
              "achieved_gbs": gbs, "frac": gbs / peak if v["bytes"] else None,
+             # nominal FFT flops (5 n log2 n per executed transform) against the measured DFMA peak
+             "fft_tflops": tfl if tfl else None,
+             "frac_fp64": tfl / f64 if (tfl and f64) else None,
              "avg_launch_us": 1e3 * v["ms"] / max(1, v["launches"])}
         if kt_step is not None and name in kt_step:
             k["ms_in_timed_step"] = kt_step[name]["ms"] / steps_step
@@ -426,6 +431,11 @@ def run_cfg2(args, world, rank, local, dev):
                      "achieved": dom["achieved_gbs"], "peak": peak, "unit": "GB/s",
                      "frac": dom["achieved_gbs"] / peak,
                      "traffic": traffic_from_profile(dom["kernel"]),
+                     "fp64": {"achieved": dom.get("fft_tflops"), "peak": (fp64_peaks() or {}).get("dfma_tflops"),
+                              "unit": "TFLOP/s", "frac": dom.get("frac_fp64"),
+                              "note": "nominal FFT flops 5 n log2 n of the dominant kernel / measured DFMA peak; "
+                                      "the far-field kernels are bound by the fp64 pipe and shared-memory "
+                                      "bandwidth, not by HBM (DESIGN.md 3)"},
                      "how": "dominant kernel family (largest exclusive time): its algorithmic bytes (executed "
                             "formulation, DESIGN.md 3) / its CUDA-event time, launches serialised on one "
                             "stream (library option serial) over %d steps right after the timed region; "

@@ -58,11 +58,12 @@ int fhtb_set_option(const char* key, int64_t value);
  * with "kernel_timing" on, every far/near launch of fhtb_apply* is bracketed
  * by CUDA events on its own stream and tagged with the algorithmic bytes it
  * moves.  fhtb_kernel_times synchronises on the recorded events, writes the
- * per-family sums (ms of event time, bytes, launches; arrays of n_fam) and
+ * per-family sums (ms of event time, bytes, nominal FFT flops at 5 n log2 n
+ * per executed n-point transform, launches; arrays of n_fam) and
  * clears the record.  Family i is named by fhtb_kernel_family_name(i). */
 int32_t fhtb_kernel_families(void);
 const char* fhtb_kernel_family_name(int32_t i);
-int fhtb_kernel_times(double* ms, double* bytes, int64_t* launches, int32_t n_fam);
+int fhtb_kernel_times(double* ms, double* bytes, double* flops, int64_t* launches, int32_t n_fam);
 
 /* ---------------------------------------------------------------- L1 --- */
 /* out[i] = J_nu(z[i]); replaces bessel.py:232-260 (bessel_j, array path). */

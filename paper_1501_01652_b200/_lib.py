@@ -55,7 +55,7 @@ EXPORTS = {
     "fhtb_set_option": (i32, [ctypes.c_char_p, i64]),
     "fhtb_kernel_families": (i32, []),
     "fhtb_kernel_family_name": (ctypes.c_char_p, [i32]),
-    "fhtb_kernel_times": (i32, [P_f64, P_f64, P_i64, i32]),
+    "fhtb_kernel_times": (i32, [P_f64, P_f64, P_f64, P_i64, i32]),
     "fhtb_bessel_j": (i32, [i32, vp, i64, vp, vp]),
     "fhtb_bessel_j_multi": (i32, [i32, vp, i64, vp, vp]),
     "fhtb_hankel_asy_eval": (i32, [i32, i32, vp, i64, vp, vp]),
@@ -156,7 +156,7 @@ def kernel_times():
     recorded since the last call (fhtb_set_option("kernel_timing", 1))."""
     lib = load()
     n = lib.fhtb_kernel_families()
-    ms, by, cnt = (ctypes.c_double * n)(), (ctypes.c_double * n)(), (ctypes.c_int64 * n)()
-    check(lib.fhtb_kernel_times(ms, by, cnt, n))
-    return {lib.fhtb_kernel_family_name(i).decode(): dict(ms=ms[i], bytes=by[i], launches=cnt[i])
+    ms, by, fl, cnt = (ctypes.c_double * n)(), (ctypes.c_double * n)(), (ctypes.c_double * n)(), (ctypes.c_int64 * n)()
+    check(lib.fhtb_kernel_times(ms, by, fl, cnt, n))
+    return {lib.fhtb_kernel_family_name(i).decode(): dict(ms=ms[i], bytes=by[i], flops=fl[i], launches=cnt[i])
             for i in range(n) if cnt[i]}

@@ -19,7 +19,7 @@ namespace fhtb {
 
 constexpr int kAsyPairs = 10;      // bessel.py:40  _ASY_TERMS
 constexpr int kTaylorTerms = 10;   // bessel.py:39  _TAYLOR_TERMS
-constexpr int kMaxOrder = 63;      // orders supported by the device tables
+constexpr int kMaxOrder = 1023;    // orders held by the per-device constant table (engine universes)
 
 // Per-order constants, filled on the host (fhtb_host.cpp).
 struct JOrder {
@@ -222,6 +222,73 @@ __device__ __forceinline__ void jn_all(int omax, double z, const JOrder* __restr
   const double inv = 1.0 / nrm;
 #pragma unroll
   for (int o = 0; o < OMAX; ++o) out[o] = (o <= omax) ? out[o] * inv : 0.0;
+}
+
+// J_{omin}..J_{omin+W-1}(z) into out[] (orders above omax are returned as 0):
+// jn_all for a window of orders that does not start at 0 (Fourier-Bessel /
+// DHT engines of order nu > 0 use the universe |nu -/+ j|, j < K).  One Miller
+// sweep: down to the window without capture, W captured steps with static
+// indices, then on to order 0 for the normalisation.
+template <int W>
+__device__ __forceinline__ void jn_window(int omin, int omax, double z, const JOrder* __restrict__ tab,
+                                           double (&out)[W]) {
+  if (z == 0.0) {
+#pragma unroll
+    for (int j = 0; j < W; ++j) out[j] = (omin + j == 0) ? 1.0 : 0.0;
+    return;
+  }
+  if (z >= tab[omax].shi) {
+    double s, co;
+    sincos(z, &s, &co);
+#pragma unroll
+    for (int j = 0; j < W; ++j) out[j] = (omin + j <= omax) ? jn_hankel_cs(z, co, s, tab[omin + j]) : 0.0;
+    return;
+  }
+  const int top = omin + W;                 // first order above the window
+  const double b = fmax((double)omax, z);
+  const int k0 = max(miller_start(b), top);
+  const double rz = 1.0 / z;
+  double up = 0.0, cur = 1e-30, nrm = 0.0;
+  // phase 1: k = k0 .. top+1 produce f_{k-1} for orders >= top (no capture)
+  for (int k = k0; k > top; --k) {
+    const double lo = fma((2.0 * k) * rz, cur, -up);
+    up = cur;
+    cur = lo;
+    if (((k - 1) & 1) == 0) nrm += 2.0 * cur;
+    if (fabs(cur) > 1e250) {
+      cur *= 1e-250; up *= 1e-250; nrm *= 1e-250;
+    }
+  }
+  // phase 2: orders top-1 .. omin, captured with static indices
+#pragma unroll
+  for (int j = W - 1; j >= 0; --j) {
+    const int o = omin + j;
+    const double lo = fma((2.0 * (o + 1)) * rz, cur, -up);
+    up = cur;
+    cur = lo;
+    out[j] = cur;
+    if ((o & 1) == 0) nrm += (o == 0) ? cur : 2.0 * cur;
+    if (fabs(cur) > 1e250) {
+      cur *= 1e-250; up *= 1e-250; nrm *= 1e-250;
+#pragma unroll
+      for (int q = j; q < W; ++q) out[q] *= 1e-250;
+    }
+  }
+  // phase 3: orders omin-1 .. 0 (normalisation only)
+  for (int o = omin - 1; o >= 0; --o) {
+    const double lo = fma((2.0 * (o + 1)) * rz, cur, -up);
+    up = cur;
+    cur = lo;
+    if ((o & 1) == 0) nrm += (o == 0) ? cur : 2.0 * cur;
+    if (fabs(cur) > 1e250) {
+      cur *= 1e-250; up *= 1e-250; nrm *= 1e-250;
+#pragma unroll
+      for (int q = 0; q < W; ++q) out[q] *= 1e-250;
+    }
+  }
+  const double inv = 1.0 / nrm;
+#pragma unroll
+  for (int j = 0; j < W; ++j) out[j] = (omin + j <= omax) ? out[j] * inv : 0.0;
 }
 
 }  // namespace fhtb

@@ -76,8 +76,9 @@ const char* const kFamNames[kNumFam] = {
 struct KtRec {
   int fam, dev;
   cudaEvent_t a, b;
-  double bytes;
+  double bytes, flops;
 };
+thread_local double t_kt_flops = 0.0;     // nominal FFT flops of the next KT launch (5 n log2 n per transform)
 std::mutex g_kt_mu;
 int g_kt_on = 0;
 std::vector<KtRec> g_kt;
@@ -99,9 +100,10 @@ cudaEvent_t kt_event(int dev) {
 struct KtScope {
   int fam, dev = 0;
   cudaStream_t st;
-  double bytes;
+  double bytes, flops;
   cudaEvent_t a = nullptr;
-  KtScope(int f, cudaStream_t s, double by) : fam(f), st(s), bytes(by) {
+  KtScope(int f, cudaStream_t s, double by) : fam(f), st(s), bytes(by), flops(t_kt_flops) {
+    t_kt_flops = 0.0;
     if (!g_kt_on) return;
     cudaGetDevice(&dev);
     a = kt_event(dev);
@@ -112,7 +114,7 @@ struct KtScope {
     cudaEvent_t b = kt_event(dev);
     if (!b || cudaEventRecord(b, st) != cudaSuccess) return;
     std::lock_guard<std::mutex> lk(g_kt_mu);
-    g_kt.push_back(KtRec{fam, dev, a, b, bytes});
+    g_kt.push_back(KtRec{fam, dev, a, b, bytes, flops});
   }
 };
 
@@ -577,7 +579,7 @@ int32_t fhtb_kernel_families(void) { return kNumFam; }
 
 const char* fhtb_kernel_family_name(int32_t i) { return (i >= 0 && i < kNumFam) ? kFamNames[i] : ""; }
 
-int fhtb_kernel_times(double* ms, double* bytes, int64_t* launches, int32_t n_fam) {
+int fhtb_kernel_times(double* ms, double* bytes, double* flops, int64_t* launches, int32_t n_fam) {
   std::vector<KtRec> recs;
   {
     std::lock_guard<std::mutex> lk(g_kt_mu);
@@ -586,6 +588,7 @@ int fhtb_kernel_times(double* ms, double* bytes, int64_t* launches, int32_t n_fa
   for (int i = 0; i < n_fam; ++i) {
     if (ms) ms[i] = 0.0;
     if (bytes) bytes[i] = 0.0;
+    if (flops) flops[i] = 0.0;
     if (launches) launches[i] = 0;
   }
   int rc = FHTB_OK;
@@ -598,6 +601,7 @@ int fhtb_kernel_times(double* ms, double* bytes, int64_t* launches, int32_t n_fa
     if (r.fam < n_fam) {
       if (ms) ms[r.fam] += t;
       if (bytes) bytes[r.fam] += r.bytes;
+      if (flops) flops[r.fam] += r.flops;
       if (launches) launches[r.fam] += 1;
     }
     std::lock_guard<std::mutex> lk(g_kt_mu);
@@ -812,6 +816,11 @@ int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
   g->orders.assign(d->orders, d->orders + d->n_orders);
   for (int o : g->orders)
     if (o < 0 || o > kMaxOrder) { delete g; return fail(FHTB_EINVAL, "order out of range"); }
+  if (*std::max_element(g->orders.begin(), g->orders.end()) - *std::min_element(g->orders.begin(), g->orders.end()) >=
+      kMaxOrd) {
+    delete g;
+    return fail(FHTB_EINVAL, "order universe spans more than 16 orders");
+  }
   g->direct = is_pow2(2 * g->L) && g->first == 1 && g->stride == 1 && g->n_out == g->L;
   if (g->direct) {
     g->logQ = ilog2ll(2 * g->L);
@@ -1535,6 +1544,38 @@ int run_exchange(const fhtb_grid* g, DevCtx* ctx, const std::vector<ReqDesc>& rs
   return FHTB_OK;
 }
 
+// Nominal FFT flops of one far-field chunk per launch (5 n log2 n per executed
+// transform of n points, zero padding included, epilogues excluded):
+// [0] first launch, [1] second, [2] third (chirp pass 3).
+void chunk_flops(const fhtb_grid* g, const FarPlan& fp, size_t ci, int npairs, double out[3]) {
+  out[0] = out[1] = out[2] = 0.0;
+  const int2 ch = fp.chunks[ci];
+  for (int u = ch.x; u < ch.y; ++u) {
+    const BlockDesc& x = g->bdesc[fp.units[u].block];
+    const double np = (double)npairs;
+    if (!g->direct) {
+      int l1, l2;
+      split_q(x.logQ, &l1, &l2);
+      const double Q = (double)(1LL << x.logQ);
+      out[0] += 2.0 * np * 5.0 * Q * l2;
+      out[1] += 2.0 * np * 2.0 * 5.0 * Q * l1;
+      out[2] += 2.0 * np * 5.0 * Q * l2;
+      continue;
+    }
+    const double Q = (double)(1LL << g->logQ);
+    if (g->logN2 == 0) {
+      out[0] += np * 5.0 * Q * g->logQ;
+    } else if (x.dmode == 1) {
+      out[0] += np * 5.0 * Q * x.dlogL1;
+    } else if (x.dmode >= 2) {
+      out[0] += np * 5.0 * Q * (g->logQ - x.dlogL1);
+    } else {
+      out[0] += np * 5.0 * Q * (g->logQ - x.dlogL1);
+      out[1] += np * 5.0 * Q * x.dlogL1;
+    }
+  }
+}
+
 // Algorithmic bytes of one far-field chunk per kernel family (kernel timing;
 // the per-unit terms of fhtb_grid_far_model_bytes, restricted to this shard's
 // pairs): [0] the first launch (pass 1 / column tables / chirp pass 1 / one
@@ -1672,10 +1713,12 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
     na.Ld = (double)g->L;
     na.n_orders = (int)g->orders.size();
     na.omax = 0;
+    na.omin = g->orders[0];
     na.orders_identity = 1;
     for (int i = 0; i < na.n_orders; ++i) {
       na.orders[i] = g->orders[i];
       na.omax = std::max(na.omax, g->orders[i]);
+      na.omin = std::min(na.omin, g->orders[i]);
       if (g->orders[i] != i) na.orders_identity = 0;
     }
     na.jtab = ctx->jtab;
@@ -1770,8 +1813,10 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
         a.logQ = g->logQ;
         a.vranges = d_ch;
         a.u0 = 0;
-        double cb[4];
+        double cb[4], cf[3];
         chunk_bytes(g, fp, 0, rs, p1 - p0, cb);
+        chunk_flops(g, fp, 0, p1 - p0, cf);
+        t_kt_flops = cf[0];
         KT(kfOnepass, st, cb[0], launch_far_onepass(a, g->logN1, (int)nu, st));
         KT(kfReduce, st, cb[3], launch_far_reduce(a, (int)nu, st));
       } else {
@@ -1791,8 +1836,9 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
           double2 *ql, *qh;
           int qb;
           if (int r = get_qtab(ctx, lq, &ql, &qh, &qb)) return r;
-          double cb[4];
+          double cb[4], cf[3];
           chunk_bytes(g, fp, ci, rs, p1 - p0, cb);
+          chunk_flops(g, fp, ci, p1 - p0, cf);
           a.qlo = ql;
           a.qhi = qh;
           a.qbits = qb;
@@ -1817,22 +1863,27 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
             }
             if (mode != 1 && g_far_prefetch) KT(kfOther, cs, 0.0, launch_prefetch_rows(a, n_units, cs));
             if (mode == 1) {
+              t_kt_flops = cf[0];
               KT(kfNarrow, cs, cb[0] + cb[1], launch_far_colgen(a, l1, n_units, cs));
             } else if (mode >= 3) {
               long long rs = 1;
               for (int u = fp.chunks[ci].x; u < fp.chunks[ci].y; ++u)
                 rs = std::max(rs, fused_rows(g, g->bdesc[fp.units[u].block], l1));
               a.rs = (int)rs;
+              t_kt_flops = cf[0];
               KT(kfRowsum, cs, cb[0], launch_far_rowsum(a, l2, mode - 3, n_units, cs));
               KT(kfRowsumFin, cs, cb[1], launch_far_rowsum_fin(a, n_units, cs));
             } else if (mode == 2) {
+              t_kt_flops = cf[0];
               KT(kfPass1, cs, cb[0], launch_far_pass1(a, l2, n_units, cs));
               int kb = 1;
               for (int u = fp.chunks[ci].x; u < fp.chunks[ci].y; ++u)
                 kb = std::max(kb, g->bdesc[fp.units[u].block].kbins);
               KT(kfRowdot, cs, cb[1], launch_far_rowdot(a, n_units, kb, cs));
             } else {
+              t_kt_flops = cf[0];
               KT(kfPass1, cs, cb[0], launch_far_pass1(a, l2, n_units, cs));
+              t_kt_flops = cf[1];
               KT(kfPass2, cs, cb[1], launch_far_pass2(a, l1, n_units, cs));
             }
             if (pipe) {
@@ -1847,9 +1898,12 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
             a.L1 = 1 << l1;
             a.L2 = 1 << l2;
             CU(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)n_units * g->n_out, st));
-            KT(kfChirp1, st, cb[0], launch_chirp_pass1(a, l2, n_units, fp.chunk_key[ci], st));
-            KT(kfChirp2, st, cb[1], launch_chirp_pass2(a, l1, n_units, st));
-            KT(kfChirp3, st, cb[2], launch_chirp_pass3(a, l2, n_units, st));
+            t_kt_flops = cf[0];
+              KT(kfChirp1, st, cb[0], launch_chirp_pass1(a, l2, n_units, fp.chunk_key[ci], st));
+            t_kt_flops = cf[1];
+              KT(kfChirp2, st, cb[1], launch_chirp_pass2(a, l1, n_units, st));
+            t_kt_flops = cf[2];
+              KT(kfChirp3, st, cb[2], launch_chirp_pass3(a, l2, n_units, st));
             KT(kfChirpReduce, st, cb[3], launch_chirp_reduce(a, n_units, st));
           }
         }
@@ -1948,11 +2002,15 @@ int fhtb_direct_apply(const fhtb_direct_desc* d, const fhtb_request* reqs, int32
   na.Ld = d->r_scale;
   na.n_orders = d->n_orders;
   na.orders_identity = 1;
+  na.omin = d->orders[0];
   for (int i = 0; i < d->n_orders; ++i) {
     na.orders[i] = d->orders[i];
     na.omax = std::max(na.omax, d->orders[i]);
+    na.omin = std::min(na.omin, d->orders[i]);
     if (d->orders[i] != i) na.orders_identity = 0;
+    if (d->orders[i] < 0 || d->orders[i] > kMaxOrder) return fail(FHTB_EINVAL, "order out of range");
   }
+  if (na.omax - na.omin >= kMaxOrd) return fail(FHTB_EINVAL, "order universe spans more than 16 orders");
   na.jtab = ctx->jtab;
     na.nf = ctx->nf;
   na.reqs = d_req;

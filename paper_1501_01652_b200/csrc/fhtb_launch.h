@@ -27,6 +27,7 @@ struct NearArgs {
   double gamma, scale, Ld;
   int n_orders, omax;
   int orders_identity;          // universe == {0, 1, ..., n_orders-1}
+  int omin;                     // smallest universe order (window [omin, omin + kMaxOrd) holds them all)
   int orders[kMaxOrd];
   const JOrder* jtab;           // indexed by order
   const ReqDesc* reqs;

@@ -151,15 +151,16 @@ near_kernel(NearArgs a) {
           // universe {0, 1, ..., n-1}: one Miller sweep of NORD orders, static indices
           jn_all<NORD>(a.omax, z, a.jtab, vals);
         } else {
+          // any universe inside a window of kMaxOrd orders [omin, omin + kMaxOrd)
           double all[kMaxOrd];
-          jn_all<kMaxOrd>(a.omax, z, a.jtab, all);
+          jn_window<kMaxOrd>(a.omin, a.omax, z, a.jtab, all);
 #pragma unroll
           for (int u = 0; u < NORD; ++u)
             if (u < a.n_orders) {
               double v = 0.0;
 #pragma unroll
               for (int o = 0; o < kMaxOrd; ++o)
-                if (o == a.orders[u]) v = all[o];
+                if (o == a.orders[u] - a.omin) v = all[o];
               vals[u] = v;
             }
         }

@@ -241,6 +241,11 @@ def _fb_apply(base_orders, C, F, n, params, inner_eps, roots, stats, prune_eps, 
     js = _JobSet(params, n, roots, n)
     bmax, nz = _high_stats(C, js.n_split, np.asarray(roots.perturbations))
     per = 2 if meta["complex"] else 1
+    if per == 2:
+        # a complex vector is two real rows; the reference plans (and prunes,
+        # fourier_bessel.py:208-225) on the complex vector: c_n != 0 if either part is
+        bmax = np.repeat(np.maximum(bmax[0::2], bmax[1::2]), 2)
+        nz = np.repeat(nz[0::2] | nz[1::2], 2)
     for v in range(C.shape[0]):
         st = stats if v % per == 0 else None
         js.add(base_orders, v, float(bmax[v]), bool(nz[v]), st, prune_eps)
@@ -254,7 +259,8 @@ def _fb_apply(base_orders, C, F, n, params, inner_eps, roots, stats, prune_eps, 
         uni = sorted(_order_universe(base_orders, params.k_terms))
         eng = SchlomilchEngine(n, -0.25, inner_eps, uni)
         eng.grid().apply(js.high, C, F)
-        eng.count(js.high_terms[:len(js.high_terms) // per] if per == 2 else js.high_terms, stats)
+        # both rows of a complex vector carry the same term lists; counted once (rows of even index)
+        eng.count([t for t, r in zip(js.high_terms, js.high) if r["vec"] % per == 0], stats)
     return F
 
 

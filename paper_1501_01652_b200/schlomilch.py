@@ -273,8 +273,58 @@ _grid_cache = collections.OrderedDict()
 _GRID_CACHE_MAX = 24
 
 
+_MAX_UNIVERSE = 16      # orders per fhtb_grid, inside a window of 16 consecutive orders (fhtb_types.h kMaxOrd)
+
+
+def _order_windows(orders):
+    """Greedy split of a sorted universe into groups one fhtb_grid can hold."""
+    out, cur = [], []
+    for o in sorted(set(int(o) for o in orders)):
+        if cur and (len(cur) >= _MAX_UNIVERSE or o - cur[0] >= _MAX_UNIVERSE):
+            out.append(cur)
+            cur = []
+        cur.append(o)
+    if cur:
+        out.append(cur)
+    return out
+
+
+class _MultiGrid:
+    """A universe wider than one fhtb_grid holds (reference engines take any
+    order set, schlomilch.py:422-431): one grid per order window, every
+    request split by its terms; far and near field are linear in the terms."""
+
+    def __init__(self, grids):
+        self.grids = grids
+        self.orders = [o for g in grids for o in g.orders]
+        self.L, self.n_out, self.m_terms, self.n_blocks = grids[0].L, grids[0].n_out, grids[0].m_terms, grids[0].n_blocks
+
+    def apply(self, requests, C, F, flags=_lib.FHTB_FAR | _lib.FHTB_NEAR):
+        for g in self.grids:
+            own = set(g.orders)
+            part = []
+            for r in requests:
+                terms = [(o, w) for o, w in r["terms"] if int(o) in own]
+                if terms:
+                    part.append(dict(r, terms=terms))
+            g.apply(part, C, F, flags)
+        return F
+
+    def apply_host(self, requests, C, F, flags=_lib.FHTB_FAR | _lib.FHTB_NEAR, n_groups=None):
+        dev = _device.device()
+        Cd = C.to(dev, non_blocking=True)
+        Fd = torch.zeros((C.shape[0], self.n_out), dtype=torch.float64, device=dev)
+        self.apply(requests, Cd, Fd, flags)
+        F.copy_(Fd)
+        return F
+
+
 def _grid(L, gamma, m_terms, blocks, segments, orders, row_first=1, row_stride=1, n_out=None,
           n_data_cols=None):
+    wins = _order_windows(orders)
+    if len(wins) > 1:
+        return _MultiGrid([_grid(L, gamma, m_terms, blocks, segments, w, row_first, row_stride, n_out, n_data_cols)
+                           for w in wins])
     key = (torch.cuda.current_device(), int(L), float(gamma), int(m_terms), tuple(blocks), tuple(segments),
            tuple(int(o) for o in orders), int(row_first), int(row_stride), n_out, n_data_cols)
     with _grid_lock:
@@ -419,6 +469,8 @@ class SchlomilchEngine:
     def apply_many(self, requests, stats=None):
         n = self.params.n
         rows, dts = [], []
+        # order_weights may be one-shot iterables (schlomilch.py:470-472 takes a tuple first)
+        requests = [(tuple(ow), c) for ow, c in requests]
         for ow, c in requests:
             for o, _ in ow:
                 if o not in self.orders:

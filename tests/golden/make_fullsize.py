@@ -389,6 +389,8 @@ def main():
     ap.add_argument("-j", type=int, default=os.cpu_count() or 1)
     ap.add_argument("--only", default="")
     ap.add_argument("--collect-only", action="store_true")
+    ap.add_argument("--merge", action="store_true",
+                    help="keep the cases already in fullsize.npz/json and add or replace the cached ones")
     a = ap.parse_args()
     os.makedirs(CACHE, exist_ok=True)
     names = [x for x in a.only.split(",") if x] or list(CASES)
@@ -400,10 +402,16 @@ def main():
             for name, how in ex.map(_run, names):
                 print(name, how, flush=True)
     meta, arrays = {}, {}
+    if a.merge:
+        with open(os.path.join(HERE, "fullsize.json")) as f:
+            meta = json.load(f)
+        with np.load(os.path.join(HERE, "fullsize.npz")) as old:
+            arrays = {k: old[k] for k in old.files}
     for name in CASES:
         p = os.path.join(CACHE, name + ".pkl")
         if not os.path.exists(p):
-            print("missing", name)
+            if name not in meta:
+                print("missing", name)
             continue
         with open(p, "rb") as f:
             m, arr = pickle.load(f)

@@ -195,3 +195,47 @@ def test_trig_any_length_vs_reference(cuda_dev, fx):
         for r in range(b):
             _check(out[r, idx], arr[key + "_val"][r], 1e-13 * l1[r], "%s %d row %d" % (kind, n, r))
             _check(out[r] @ w, arr[key + "_chk"][r], 1e-13 * l1[r] * np.abs(w).sum(), "%s %d checksum" % (kind, n))
+
+
+def test_high_orders_vs_reference(cuda_dev, fx):
+    """Orders beyond the round-1 caps (reference engines take any integer
+    nu >= 0, schlomilch.py:422-431, bessel.py:232-260): Schlomilch nu = 64..100,
+    Fourier-Bessel nu = 20 and 60 (universes |nu -/+ j| up to order 65, i.e.
+    windows that do not start at order 0), bessel_j up to nu = 150."""
+    meta, arr = fx
+    for case in meta["high_order"]["cases"]:
+        key = "high_order/" + case["key"]
+        if case["kind"] == "bessel":
+            nu = case["nu"]
+            z = arr["high_order/bj_z_%d" % nu]
+            # 1e-14 plus the reference's own phase rounding at large z (ulp(z)/2 rad times
+            # the envelope, see test_bessel_large_arguments_vs_reference)
+            tol = 1e-14 + np.spacing(z) * np.sqrt(2.0 / (np.pi * np.maximum(z, 1.0)))
+            bad = np.abs(fh.bessel_j(nu, z) - arr[key]) > tol
+            assert not bad.any(), (nu, z[bad][:5])
+        elif case["kind"] == "schlomilch":
+            nu, n, eps = case["nu"], case["n"], case["eps"]
+            c = np.random.default_rng([80, nu, n]).standard_normal(n)
+            f = fh.schlomilch_fast(fh.select_params(nu, n, eps), c)
+            _check(f, arr[key], 10 * eps * np.abs(c).sum(), "schlomilch nu=%d N=%d" % (nu, n))
+        else:
+            nu, n, eps = case["nu"], case["n"], case["eps"]
+            c = np.random.default_rng([81, nu, n]).uniform(-1, 1, n)
+            f = fh.fourier_bessel_eval(nu, c, eps)
+            _check(f, arr[key], 10 * eps * np.abs(c).sum(), "fourier_bessel nu=%d N=%d" % (nu, n))
+
+
+def test_engine_universe_wider_than_one_grid(cuda_dev):
+    """An engine universe of more than 16 orders (or spread over more than 16
+    consecutive orders) is served by one grid per order window; the result is
+    the sum of the single-order evaluations."""
+    n, eps = 1500, 1e-12
+    orders = list(range(0, 40, 2)) + [70]
+    rng = np.random.default_rng(5)
+    c = rng.standard_normal(n)
+    w = rng.uniform(0.5, 1.5, len(orders))
+    from paper_1501_01652_b200.schlomilch import SchlomilchEngine
+    eng = SchlomilchEngine(n, 0.0, eps, orders)
+    got = eng.apply(tuple(zip(orders, w)), c)
+    want = sum(wi * fh.schlomilch_direct(o, 0.0, c) for o, wi in zip(orders, w))
+    assert np.max(np.abs(got - want)) <= 10 * eps * np.abs(c).sum() * np.abs(w).sum()
