@@ -66,6 +66,15 @@ const char* fhtb_kernel_family_name(int32_t i);
 int fhtb_kernel_times(double* ms, double* bytes, double* flops, int64_t* launches, int32_t n_fam);
 
 /* ---------------------------------------------------------------- L1 --- */
+/* Planning statistics of coefficient rows C[v][0..n) on the device, returned
+ * to the host (synchronises `stream`): out_host[3v] = sum |c|, [3v+1] = max
+ * |b[i]| over i >= n_split with c[i] != 0 (b: nb device values, may be null),
+ * [3v+2] = 1 if any such i.  Replaces the numpy scans of
+ * fourier_bessel.py:208-225 and dht.py:140-157 (norm1, b_max, nonzero). */
+int fhtb_coef_stats(const double* C, int64_t ldc, int32_t n_vec, int64_t n, int64_t n_split, const double* b,
+                    int64_t nb, double* out_host, void* stream);
+/* F[v][0..n) = 0 for v < n_vec (stream-ordered memset of result rows). */
+int fhtb_zero_rows(double* F, int64_t ldf, int32_t n_vec, int64_t n, void* stream);
 /* out[i] = J_nu(z[i]); replaces bessel.py:232-260 (bessel_j, array path). */
 int fhtb_bessel_j(int nu, const double* z, int64_t n, double* out, void* stream);
 /* out[o*n + i] = J_o(z[i]) for o <= nu_max (one Miller sweep). */

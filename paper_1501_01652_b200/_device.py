@@ -6,6 +6,7 @@ libfhtb200.so.
 """
 
 import contextlib
+import ctypes
 import threading
 
 import numpy as np
@@ -97,6 +98,28 @@ def workspace(nbytes):
             buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
             _ws[key] = buf
     return buf
+
+
+def zeros_like(C):
+    """A zeroed result matrix shaped like C (library memset on the current stream)."""
+    F = torch.empty_like(C)
+    if F.numel():
+        _lib.call("fhtb_zero_rows", ptr(F), F.stride(0) if F.ndim == 2 else F.numel(),
+                  F.shape[0] if F.ndim == 2 else 1, F.shape[-1], stream_ptr())
+    return F
+
+
+def coef_stats(C, n_split=0, b_dev=None):
+    """Per row of the (B, N) device matrix C: (sum |c|, max |b_n| over the
+    n >= n_split with c_n != 0, any such n) -- one library kernel and one
+    small copy instead of a chain of eager tensor ops."""
+    out = np.zeros((C.shape[0], 3))
+    if C.shape[0]:
+        nb = 0 if b_dev is None else int(b_dev.numel())
+        _lib.call("fhtb_coef_stats", ptr(C), C.stride(0), C.shape[0], C.shape[1], int(n_split),
+                  ptr(b_dev) if b_dev is not None else None, nb,
+                  out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), stream_ptr())
+    return out[:, 0], out[:, 1], out[:, 2] > 0
 
 
 def to_dev_f64(x, dev=None):

@@ -51,6 +51,8 @@ EXPORTS = {
     "fhtb_last_error": (ctypes.c_char_p, []),
     "fhtb_launch_count": (i64, []),
     "fhtb_nonfinite_check": (i32, [vp]),
+    "fhtb_coef_stats": (i32, [vp, i64, i32, i64, i64, vp, i64, P_f64, vp]),
+    "fhtb_zero_rows": (i32, [vp, i64, i32, i64, vp]),
     "fhtb_init": (i32, []),
     "fhtb_set_option": (i32, [ctypes.c_char_p, i64]),
     "fhtb_kernel_families": (i32, []),

@@ -785,6 +785,28 @@ int fhtb_roots_j0(int64_t count, double* roots, double* perturb, double* resid_m
   return FHTB_OK;
 }
 
+int fhtb_coef_stats(const double* C, int64_t ldc, int32_t n_vec, int64_t n, int64_t n_split, const double* b,
+                    int64_t nb, double* out_host, void* stream) {
+  if (n_vec < 0 || n < 0 || n_split < 0 || !out_host) return fail(FHTB_EINVAL, "bad coef_stats arguments");
+  if (n_vec == 0) return FHTB_OK;
+  DevCtx* c;
+  if (int r = get_ctx(&c)) return r;
+  double* d = nullptr;
+  CU(cudaMallocAsync((void**)&d, sizeof(double) * 3 * (size_t)n_vec, S(stream)));
+  CU(launch_coef_stats(C, ldc, n_vec, n, n_split, b, nb, d, S(stream)));
+  CU(cudaMemcpyAsync(out_host, d, sizeof(double) * 3 * (size_t)n_vec, cudaMemcpyDeviceToHost, S(stream)));
+  CU(cudaFreeAsync(d, S(stream)));
+  CU(cudaStreamSynchronize(S(stream)));
+  return FHTB_OK;
+}
+
+int fhtb_zero_rows(double* F, int64_t ldf, int32_t n_vec, int64_t n, void* stream) {
+  if (n_vec < 0 || n < 0 || ldf < n) return fail(FHTB_EINVAL, "bad zero_rows arguments");
+  if (n_vec == 0 || n == 0) return FHTB_OK;
+  CU(cudaMemset2DAsync(F, sizeof(double) * (size_t)ldf, 0, sizeof(double) * (size_t)n, (size_t)n_vec, S(stream)));
+  return FHTB_OK;
+}
+
 int fhtb_fft(int64_t n, int sign, const double* in, double* out, int64_t batch, void* stream) {
   if (!is_pow2(n) || n < 2 || n > 2048) return fail(FHTB_EINVAL, "fhtb_fft: n must be a power of two in [2, 2048]");
   DevCtx* c;

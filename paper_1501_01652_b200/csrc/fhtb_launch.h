@@ -142,6 +142,8 @@ cudaError_t launch_hankel_eval(int nu, int m_terms, const double* coef, const do
                                double* out, cudaStream_t st);
 cudaError_t launch_taylor_eval(int nu, int n_terms, double inv_fact, const double* z, long long n,
                                double* out, cudaStream_t st);
+cudaError_t launch_coef_stats(const double* C, long long ldc, int n_vec, long long n, long long n_split,
+                              const double* b, long long nb, double* out, cudaStream_t st);
 cudaError_t launch_roots_j0(const JOrder* tab, long long count, double* roots, double* pert,
                             unsigned long long* resid_bits, cudaStream_t st);
 cudaError_t launch_fft_batch(int logN, int sign, const double2* in, double2* out, long long batch,

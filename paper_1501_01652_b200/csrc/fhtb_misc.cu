@@ -176,6 +176,46 @@ cudaError_t launch_fft_batch(int logN, int sign, const double2* in, double2* out
   return cudaErrorInvalidValue;
 }
 
+// Planning statistics of one coefficient row (fourier_bessel.py:208-225,
+// dht.py:140-157 take them with numpy on the host): out[3v] = sum |c_n|,
+// out[3v+1] = max |b_n| over the n >= n_split with c_n != 0, out[3v+2] = 1 if
+// any such n exists.  One CTA per row, fixed-order tree (deterministic).
+__global__ void __launch_bounds__(256)
+coef_stats_kernel(const double* __restrict__ C, long long ldc, long long n, long long n_split,
+                  const double* __restrict__ b, long long nb, double* __restrict__ out) {
+  const double* c = C + (long long)blockIdx.x * ldc;
+  double l1 = 0.0, bm = 0.0, nz = 0.0;
+  for (long long i = threadIdx.x; i < n; i += 256) {
+    const double x = c[i];
+    l1 += fabs(x);
+    if (i >= n_split && x != 0.0) {
+      nz = 1.0;
+      if (b && i < nb) bm = fmax(bm, fabs(b[i]));
+    }
+  }
+  __shared__ double s[3][256];
+  s[0][threadIdx.x] = l1;
+  s[1][threadIdx.x] = bm;
+  s[2][threadIdx.x] = nz;
+  __syncthreads();
+  for (int h = 128; h; h >>= 1) {
+    if (threadIdx.x < h) {
+      s[0][threadIdx.x] += s[0][threadIdx.x + h];
+      s[1][threadIdx.x] = fmax(s[1][threadIdx.x], s[1][threadIdx.x + h]);
+      s[2][threadIdx.x] = fmax(s[2][threadIdx.x], s[2][threadIdx.x + h]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < 3) out[3 * (long long)blockIdx.x + threadIdx.x] = s[threadIdx.x][0];
+}
+
+cudaError_t launch_coef_stats(const double* C, long long ldc, int n_vec, long long n, long long n_split,
+                              const double* b, long long nb, double* out, cudaStream_t st) {
+  if (n_vec == 0) return cudaSuccess;
+  note_launch(), coef_stats_kernel<<<n_vec, 256, 0, st>>>(C, ldc, n, n_split, b, nb, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_twiddles(double2* pool, int max_log, cudaStream_t st) {
   const long long total = (1LL << (max_log + 1)) - 2;
   note_launch(), twiddle_kernel<<<grid_for(total, 256), 256, 0, st>>>(pool, max_log);

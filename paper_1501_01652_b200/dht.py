@@ -79,7 +79,7 @@ def dht_direct(plan, c):
     if c_arr.shape[-1] != plan.n:
         raise ValueError("coefficient length does not match plan.n")
     C, meta = _device.as_real_batch(c_arr)
-    F = torch.zeros_like(C)
+    F = _device.zeros_like(C)
     _rows_direct(plan, C, F, plan.n + 1)
     return _device.from_real_batch(F, meta)
 
@@ -112,7 +112,7 @@ def dht(plan, c, stats=None):
         raise ValueError("coefficient length does not match plan.n")
     C, meta = _device.as_real_batch(c_arr)
     per = 2 if meta["complex"] else 1
-    F = torch.zeros_like(C)
+    F = _device.zeros_like(C)
     split = min(plan.row_split, n)
     if split >= n:
         _rows_direct(plan, C, F, n + 1, stats, per)
@@ -121,13 +121,13 @@ def dht(plan, c, stats=None):
     fbp, eng = sh["fb"], sh["engine"]
     n_pad = 4 * n + 3
     r_dev, _ = plan.roots.device_arrays()
-    norm1 = C.abs().sum(dim=1).cpu().numpy()
     g_max = 1.01 / (8.0 * (split + 0.75) * math.pi)
     js = _JobSet(fbp, n_pad, plan.roots, n)
     support = min(n_pad, plan.roots.n_max)
     if support < n:
         raise ValueError("roots table too short for the coefficient support")
-    bmax, nz = _high_stats(C, js.n_split, np.asarray(plan.roots.perturbations))
+    _, b_dev = plan.roots.device_arrays()
+    norm1, bmax, nz = _device.coef_stats(C, js.n_split, b_dev)
     K, T = plan.k_terms, plan.t_terms
     for v in range(C.shape[0]):
         st = stats if v % per == 0 else None

@@ -199,17 +199,12 @@ class _JobSet:
         _bump(stats, "pointwise_evaluations", len(orders) * self.n_grid * self.n_split)
 
 
-def _high_stats(C_rows, n_split, b_host):
-    """Per-vector (bmax, nonzero) of the high part c[n_split:] (planning only)."""
-    if isinstance(C_rows, torch.Tensor):
-        nzm = (C_rows[:, n_split:] != 0)
-        bb = torch.from_numpy(np.abs(b_host[n_split:C_rows.shape[1]])).to(C_rows.device)
-        if bb.numel() < nzm.shape[1]:
-            bb = torch.cat([bb, bb.new_zeros(nzm.shape[1] - bb.numel())])
-        bm = (nzm * bb).amax(dim=1) if nzm.shape[1] else torch.zeros(C_rows.shape[0], dtype=torch.float64)
-        anyz = nzm.any(dim=1) if nzm.shape[1] else torch.zeros(C_rows.shape[0], dtype=torch.bool)
-        return bm.cpu().numpy(), anyz.cpu().numpy()
-    raise TypeError("expected a tensor")
+def _high_stats(C_rows, n_split, roots):
+    """Per-vector (bmax, nonzero) of the high part c[n_split:] (planning only):
+    one library reduction (fhtb_coef_stats) and one small copy."""
+    _, b_dev = roots.device_arrays()
+    _, bm, anyz = _device.coef_stats(C_rows, n_split, b_dev)
+    return bm, anyz
 
 
 def fourier_bessel_eval(nu, c, eps, roots=None, stats=None, prune=False):
@@ -229,7 +224,7 @@ def fourier_bessel_eval(nu, c, eps, roots=None, stats=None, prune=False):
         roots = bessel_roots_j0(n)
     inner_eps = eps / (2 * params.t_terms + params.k_terms - 2)
     C, meta = _device.as_real_batch(c_arr)
-    F = torch.zeros_like(C)
+    F = _device.zeros_like(C)
     _fb_apply(((nu, 1.0),), C, F, n, params, inner_eps, roots, stats, eps if prune else None, meta)
     return _device.from_real_batch(F, meta)
 
@@ -239,7 +234,7 @@ def _fb_apply(base_orders, C, F, n, params, inner_eps, roots, stats, prune_eps, 
     if support < n and bool((C[:, support:] != 0).any()):
         raise ValueError("roots table too short for the coefficient support")
     js = _JobSet(params, n, roots, n)
-    bmax, nz = _high_stats(C, js.n_split, np.asarray(roots.perturbations))
+    bmax, nz = _high_stats(C, js.n_split, roots)
     per = 2 if meta["complex"] else 1
     if per == 2:
         # a complex vector is two real rows; the reference plans (and prunes,
@@ -276,7 +271,7 @@ def neumann_matvec(nu, c, params, schlomilch_eps, roots=None, stats=None):
     if np.any(c_arr[support:]):
         raise ValueError("roots table too short for the coefficient support")
     C, meta = _device.as_real_batch(c_arr)
-    F = torch.zeros_like(C)
+    F = _device.zeros_like(C)
     _, b_dev = roots.device_arrays()
     top = 2 * params.t_terms + params.k_terms - 2
     reqs, terms_l = [], []
@@ -301,7 +296,7 @@ def fourier_bessel_direct(nu, c, roots=None):
     if roots is None:
         roots = bessel_roots_j0(n)
     C, meta = _device.as_real_batch(c_arr)
-    F = torch.zeros_like(C)
+    F = _device.zeros_like(C)
     r_dev, _ = roots.device_arrays()
     rows = _row_grid(n, 1, 1, n, C.device)
     reqs = [dict(vec=v, terms=[(int(nu), 1.0)]) for v in range(C.shape[0])]

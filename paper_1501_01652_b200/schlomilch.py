@@ -374,7 +374,7 @@ def _run(params, scheme, order_weights, c, stats, flags=_lib.FHTB_FAR | _lib.FHT
         raise ValueError("coefficient length does not match params.n")
     orders = sorted({int(o) for o, _ in order_weights})
     g = _grid(params.n, params.gamma, params.m_terms, scheme.blocks, scheme.mask_segments, orders)
-    F = torch.zeros_like(C)
+    F = _device.zeros_like(C)
     reqs = [dict(vec=v, terms=list(order_weights)) for v in range(C.shape[0])]
     g.apply(reqs, C, F, flags)
     nvec = C.shape[0] // (2 if meta["complex"] else 1)
@@ -485,7 +485,7 @@ class SchlomilchEngine:
         cplx = any(np.iscomplexobj(r) for r in rows)
         mat = np.stack([r.astype(np.complex128 if cplx else np.float64) for r in rows])
         C, meta = _device.as_real_batch(mat)
-        F = torch.zeros_like(C)
+        F = _device.zeros_like(C)
         per = 2 if cplx else 1
         reqs = []
         for i, (ow, _) in enumerate(requests):
