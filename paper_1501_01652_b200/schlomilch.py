@@ -194,7 +194,7 @@ class _Grid:
     HOST_GROUPS = 8
     HOST_GROUP_MIN_VECS = 8
 
-    def apply_host(self, requests, C, F, flags=_lib.FHTB_FAR | _lib.FHTB_NEAR, n_groups=None):
+    def apply_host(self, requests, C, F, flags=_lib.FHTB_FAR | _lib.FHTB_NEAR, n_groups=None, sync=True):
         """F = application of the requests, C and F pinned host float64
         tensors (B, n_data_cols) / (B, n_out): fhtb_apply_host, the copies
         overlapped with the far field in vector groups.  Same bits as
@@ -207,7 +207,8 @@ class _Grid:
         _lib.check(self._lib.fhtb_apply_host(self.handle, arr, len(requests), C.data_ptr(), C.stride(0),
                                              C.shape[0], F.data_ptr(), F.stride(0), flags, int(n_groups),
                                              _device.ptr(ws), ws.numel(), _device.stream_ptr()))
-        torch.cuda.current_stream().synchronize()
+        if sync:
+            torch.cuda.current_stream().synchronize()
         del keep
         return F
 
@@ -352,8 +353,107 @@ def _host_pinned_real(c):
             and c.ndim in (1, 2) and c.is_contiguous() and c.is_pinned() and _device.shard()[1] == 1)
 
 
+# numpy in / numpy out (the reference's calling convention) for large real
+# batches: pageable memory cannot be copied asynchronously, so the rows are
+# staged through pinned buffers (three slots) in vector chunks -- worker
+# threads copy chunk i+1 in and chunk i-1 out (numpy copies release the GIL)
+# while the GPU runs chunk i; consecutive chunks alternate between two CUDA
+# streams so that one chunk's copy-out overlaps the next one's far field.
+_NP_PIPE_MIN_ELEMS = 1 << 22
+_NP_PIPE_THREADS = 4            # host copy workers (a fresh result array is first touched by the copy-out)
+_np_pipe_lock = threading.Lock()
+_np_pipe = {}
+
+
+def _np_pipe_state(rows, n, n_out):
+    key = (torch.cuda.current_device(), rows, n, n_out)
+    st = _np_pipe.get(key)
+    if st is None:
+        import concurrent.futures
+        _np_pipe.clear()                                   # one shape at a time (pinned memory is scarce)
+        st = dict(pin_in=[torch.empty((rows, n), dtype=torch.float64, pin_memory=True) for _ in range(3)],
+                  pin_out=[torch.empty((rows, n_out), dtype=torch.float64, pin_memory=True) for _ in range(3)],
+                  streams=[torch.cuda.Stream() for _ in range(2)],
+                  pool=concurrent.futures.ThreadPoolExecutor(_NP_PIPE_THREADS))
+        _np_pipe[key] = st
+    return st
+
+
+def _run_numpy_pipelined(g, order_weights, c2, flags):
+    B, n = c2.shape
+    rows = 8 if B >= 16 else max(1, (B + 1) // 2)
+    n_out = g.n_out
+    out = np.empty((B, n_out))
+    with _np_pipe_lock:
+        st = _np_pipe_state(rows, n, n_out)
+        pin_in, pin_out, streams, pool = st["pin_in"], st["pin_out"], st["streams"], st["pool"]
+        chunks = [(lo, min(B, lo + rows)) for lo in range(0, B, rows)]
+        np_in = [t.numpy() for t in pin_in]
+        np_out = [t.numpy() for t in pin_out]
+
+        class _Many:
+            def __init__(self, fs):
+                self.fs = fs
+
+            def result(self):
+                for f in self.fs:
+                    f.result()
+
+        def halves(lo, hi):
+            mid = (lo + hi + 1) // 2
+            return [(lo, mid), (mid, hi)] if hi - lo > 1 else [(lo, hi)]
+
+        def stage_in(i):
+            lo, hi = chunks[i]
+            return _Many([pool.submit(np.copyto, np_in[i % 3][a - lo: b - lo], c2[a:b]) for a, b in halves(lo, hi)])
+
+        def stage_out(i):
+            lo, hi = chunks[i]
+            return _Many([pool.submit(np.copyto, out[a:b], np_out[i % 3][a - lo: b - lo]) for a, b in halves(lo, hi)])
+
+        cur = torch.cuda.current_stream()
+        for s_ in streams:
+            s_.wait_stream(cur)
+        f_in = {0: stage_in(0)}
+        f_out, done = {}, {}
+        for i, (lo, hi) in enumerate(chunks):
+            if i + 1 < len(chunks):
+                f_in[i + 1] = stage_in(i + 1)              # slot (i+1) % 3: chunk i-2 was waited for at step i-1
+            f_in[i].result()
+            if i >= 3:
+                f_out[i - 3].result()                      # pin_out[i % 3] is free again
+            reqs = [dict(vec=v, terms=list(order_weights)) for v in range(hi - lo)]
+            with torch.cuda.stream(streams[i % 2]):
+                g.apply_host(reqs, pin_in[i % 3][: hi - lo], pin_out[i % 3][: hi - lo], flags, sync=False)
+                done[i] = torch.cuda.Event()
+                done[i].record()
+            if i >= 1:
+                done[i - 1].synchronize()
+                f_out[i - 1] = stage_out(i - 1)
+        last = len(chunks) - 1
+        done[last].synchronize()
+        f_out[last] = stage_out(last)
+        for f in f_out.values():
+            f.result()
+        cur.wait_stream(streams[0])
+        cur.wait_stream(streams[1])
+    return out
+
+
 def _run(params, scheme, order_weights, c, stats, flags=_lib.FHTB_FAR | _lib.FHTB_NEAR):
     """Apply the partitioned scheme to c (vector, batch or tensor)."""
+    if (isinstance(c, np.ndarray) and c.dtype == np.float64 and c.ndim == 2 and c.shape[0] >= 4
+            and c.size >= _NP_PIPE_MIN_ELEMS and _device.shard()[1] == 1 and c.shape[-1] == params.n):
+        _device.ensure_init()
+        orders = sorted({int(o) for o, _ in order_weights})
+        g = _grid(params.n, params.gamma, params.m_terms, scheme.blocks, scheme.mask_segments, orders)
+        if isinstance(g, _Grid):
+            F = _run_numpy_pipelined(g, order_weights, c, flags)
+            if flags & _lib.FHTB_FAR:
+                _bump(stats, "transform_applications", c.shape[0] * 2 * params.m_terms * len(scheme.blocks))
+            if flags & _lib.FHTB_NEAR:
+                _bump(stats, "pointwise_evaluations", c.shape[0] * scheme.mask_size() * len(order_weights))
+            return F
     if _host_pinned_real(c):
         if c.shape[-1] != params.n:
             raise ValueError("coefficient length does not match params.n")

@@ -143,3 +143,27 @@ def test_self_inverse(fh, golden):
     for rec in meta["selfinv"]:
         r = fh.dht_self_inverse_residual(rec["n"], rec["eps"], A["selfinv_%d_c" % rec["i"]])
         assert abs(r - rec["residual"]) <= 1e-10 + 1e-3 * rec["residual"]
+
+
+def test_numpy_batch_pipeline_matches_device_path(fh, cuda_dev):
+    """Large numpy batches take the pinned-staging pipeline (schlomilch.py
+    _run_numpy_pipelined: chunks of vectors on two streams, host copies on
+    worker threads); same bits as the device-resident application, any batch
+    size (ragged last chunk, odd counts)."""
+    import torch
+    n = 2 ** 18
+    params = fh.select_params(4, n, 1e-15, gamma=4.0)
+    for B in (16, 21, 4):
+        if B * n < (1 << 22):
+            continue
+        c = np.random.default_rng([31, B]).standard_normal((B, n)) / np.arange(1, n + 1)
+        got = fh.schlomilch_fast(params, c)
+        want = fh.schlomilch_fast(params, torch.from_numpy(c).to(cuda_dev)).cpu().numpy()
+        assert isinstance(got, np.ndarray) and got.shape == (B, n)
+        assert np.array_equal(got, want)
+    st = {}
+    c = np.random.default_rng(32).standard_normal((16, n))
+    fh.schlomilch_fast(params, c, stats=st)
+    st2 = {}
+    fh.schlomilch_fast(params, torch.from_numpy(c).to(cuda_dev), stats=st2)
+    assert st == st2
