@@ -693,15 +693,15 @@ def bounds_from_profile():
         return None
 
 
-def traffic_from_profile(kernel):
+def traffic_from_profile(kernel, batch=BATCH):
     """ncu dram__bytes_read.sum + dram__bytes_write.sum per step of the
     kernel family (profiles/traffic.json, tools/traffic.py), or None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
             t = json.load(f)
-        fam = t.get("per_family_dram_bytes_per_step", {})
-        return fam.get(kernel)
+        v = t.get("per_family_dram_bytes_per_vector", {}).get(kernel)
+        return None if v is None else v * batch
     except Exception:
         return None
 

@@ -62,10 +62,10 @@ __device__ __forceinline__ void pair_inputs(int p, const double (&u)[EH], const 
   extra = make_double2(us, (us * iws) * sig);
 }
 
-template <int N2, int W, int MINB>
-__global__ void __launch_bounds__(W * (N2 / 16), MINB)
+template <int N2, int W, int MINB, int E = 16>
+__global__ void __launch_bounds__(W * (N2 / E), MINB)
 far_rowsum_kernel(FarArgs a) {
-  constexpr int E = 16, T = N2 / E, EH = E / 2, NTH = W * T;
+  constexpr int T = N2 / E, EH = E / 2, NTH = W * T;
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
   constexpr int NP = N2 + PAD;
   extern __shared__ __align__(16) double2 sm2[];
@@ -308,12 +308,12 @@ far_rowsum_fin_kernel(FarArgs a) {
   a.part[(long long)ul * a.part_stride + (k - 1)] = v;
 }
 
-template <int N2, int W, int MINB>
+template <int N2, int W, int MINB, int E = 16>
 static cudaError_t rowsum_t(const FarArgs& a, int n_units, cudaStream_t st) {
-  constexpr int T = N2 / 16, NTH = W * T;
+  constexpr int T = N2 / E, NTH = W * T;
   constexpr int PAD = 8 / W > 0 ? 8 / W : 0;
-  const int smem = W * (N2 + PAD) * 16 + 16 * NTH * (8 + 8 + 16);   // FFT buffers + L/k tables + second accumulators
-  auto k = far_rowsum_kernel<N2, W, MINB>;
+  const int smem = W * (N2 + PAD) * 16 + E * NTH * (8 + 8 + 16);   // FFT buffers + L/k tables + second accumulators
+  auto k = far_rowsum_kernel<N2, W, MINB, E>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   if (a.L1 % W) return cudaErrorInvalidValue;
@@ -359,7 +359,11 @@ cudaError_t launch_far_rowsum(const FarArgs& a, int logN2, int form, int n_units
     case 9: return rowsum_t<512, 4, 2>(a, n_units, st);
     case 10: return rowsum_t<1024, 2, 2>(a, n_units, st);
     case 11: return rowsum_t<2048, 1, 2>(a, n_units, st);
-    case 12: return rowsum_t<4096, 1, 1>(a, n_units, st);
+    case 12:
+      // 8 points per thread: 512 threads (16 warps) on the one CTA an SM holds,
+      // one more shared-memory exchange (variant bit 17 selects 16 points, 8 warps)
+      if (g_far_variant & 0x20000) return rowsum_t<4096, 1, 1>(a, n_units, st);
+      return rowsum_t<4096, 1, 1, 8>(a, n_units, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -1,5 +1,3 @@
-# far-field variant sweep (FHTB_FAR_VARIANT bit fields, fhtb_far.cu) on the cfg2 far field
 base=$((4 + (1<<4) + (3<<20)))
-for v in $base $((4 + (1<<4) + (1<<20))) $((4 + (1<<4) + (2<<20))) $((4 + (1<<4) + (4<<20))) $((4 + (2<<4) + (3<<20))) $((4 + (3<<4) + (3<<20))) $((4 + (4<<4) + (3<<20))) $((1 + (1<<4) + (3<<20))) $((5 + (1<<4) + (3<<20))); do
-  FHTB_FAR_VARIANT=$v python tools/time_apply.py --reps 5 | cut -c1-120
-done
+for r in 1 2; do for v in $base $((base + (1<<17))); do FHTB_FAR_VARIANT=$v python tools/time_apply.py --reps 5 | cut -c1-110; done; done
+python -m pytest tests/test_gpu_options.py tests/test_gpu_fullsize_ref.py -m gpu -q 2>&1 | tail -2

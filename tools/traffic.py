@@ -26,7 +26,29 @@ def main(path, batch, model, out):
         tot += v
         short = name.replace("fhtb::", "").replace("(int)", "").replace("(bool)", "").split("(")[0]
         per[short] = per.get(short, 0.0) + v
-    res = {"source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over every far-field kernel of one "
+    def family(k):
+        if "far_pass1" in k:
+            return "far_pass1"
+        if "far_rowsum_fin" in k:
+            return "far_rowsum_fin"
+        if "far_rowsum" in k:
+            return "far_rowsum"
+        if "far_rowdot" in k:
+            return "far_rowdot"
+        if "far_reduce" in k:
+            return "far_reduce"
+        if "colgen" in k:
+            return "far_narrow_cols"
+        if "far_pass2" in k:
+            args = k[k.index("<") + 1:k.index(">")].replace(" ", "").split(",") if "<" in k else []
+            return "far_narrow_cols" if len(args) > 2 and args[2] == "2" else "far_pass2"
+        return "other"
+
+    fam = {}
+    for k, v in per.items():
+        fam[family(k)] = fam.get(family(k), 0.0) + v / batch
+    res = {"per_family_dram_bytes_per_vector": fam,
+           "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over every far-field kernel of one "
                      "cfg2 far-field call (%d vectors), %s" % (batch, path),
            "far_field_dram_bytes_per_vector": tot / batch,
            "model_bytes_per_vector": model,
