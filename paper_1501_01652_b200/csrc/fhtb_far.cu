@@ -223,7 +223,12 @@ far_pass1p_kernel(FarArgs a) {
 #define TQS_ON(MODE, E, MINB) ((MODE) == 2 && ((E) >= 16 || (MINB) >= 5))
 #define TQS_SMEM(MODE, E) ((MODE) == 2 && (E) >= 16)
 #define IRS_K(E, MODE) false
-template <int N1, int E, int MODE, int MINB>
+// narrow-column blocks: the Horner accumulators live in thread-private shared-memory
+// slots (read-modify-write once per pair and row) instead of NQ complex registers;
+// at the register caps of these shapes (128 at 2048 points, 96 at 512) ncu counted
+// as many local (spill) loads and stores as global loads (variant bit 18 turns it off)
+// (template parameter ACS of the kernel)
+template <int N1, int E, int MODE, int MINB, bool ACS = false>
 __global__ void __launch_bounds__((MODE == 1 ? 1 : 2) * (N1 / E), MINB)
 far_pass2_kernel(FarArgs a) {
   constexpr bool ONEPASS = (MODE == 1);
@@ -261,11 +266,13 @@ far_pass2_kernel(FarArgs a) {
   // IRS (E = 16, Horner modes): the row factors L/k live in shared memory
   // ([q][tid] after the FFT buffers) instead of NQ registers, which the
   // 16-point state cannot spare without spilling
-  constexpr bool IRS = false;   // (measured: 18.05 -> 18.30 ms at 2048 points, so off)
+  constexpr bool IRS = false;   // (measured: 18.05 -> 18.30 ms at 2048 points; with the accumulators in shared memory 64.5 -> 66.6 ms far field, so off)
   double* irs = reinterpret_cast<double*>(sm2 + NCOL * NP + (TQS_ON(MODE, E, MINB) ? NCOL * E : 0));
   int* kqs = reinterpret_cast<int*>(irs + (IRS ? NQ * NT : 0));      // IRS: row indices too
   double ir[IRS ? 1 : NQ], rp[HOR ? 1 : NQ];
-  double2 acc[NQ];
+  constexpr bool ACSC = ACS, acs = ACS;
+  double2* accs = reinterpret_cast<double2*>(kqs + (IRS ? NQ * NT : 0)) + tid;   // [q * NT]
+  double2 acc[ACS ? 1 : NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int o = tid + NT * q;
@@ -279,7 +286,8 @@ far_pass2_kernel(FarArgs a) {
     }
     if (IRS) kqs[q * NT + tid] = k;
     else kq[IRS ? 0 : q] = k;
-    acc[q] = make_double2(0.0, 0.0);
+    if (ACS) accs[q * NT] = make_double2(0.0, 0.0);
+    else acc[ACS ? 0 : q] = make_double2(0.0, 0.0);
     const double irq = k ? a.Ld / (double)k : 0.0;
     if (IRS) irs[q * NT + tid] = irq;
     else ir[IRS ? 0 : q] = irq;
@@ -401,12 +409,19 @@ far_pass2_kernel(FarArgs a) {
       const double w = IRS ? irs[q * NT + tid] : ir[IRS ? 0 : q];
       if (HOR) {
         const double w2 = w * w;
-        acc[q].x = fma(acc[q].x, w2, fma(w, t1x, t0x));
-        acc[q].y = fma(acc[q].y, w2, fma(w, t1y, t0y));
+        if (ACSC && acs) {
+          double2 t = accs[q * NT];
+          t.x = fma(t.x, w2, fma(w, t1x, t0x));
+          t.y = fma(t.y, w2, fma(w, t1y, t0y));
+          accs[q * NT] = t;
+        } else {
+          acc[ACS ? 0 : q].x = fma(acc[ACS ? 0 : q].x, w2, fma(w, t1x, t0x));
+          acc[ACS ? 0 : q].y = fma(acc[ACS ? 0 : q].y, w2, fma(w, t1y, t0y));
+        }
       } else {
         const double r0 = rp[HOR ? 0 : q], r1 = r0 * w;
-        acc[q].x = fma(r0, t0x, fma(r1, t1x, acc[q].x));
-        acc[q].y = fma(r0, t0y, fma(r1, t1y, acc[q].y));
+        acc[ACS ? 0 : q].x = fma(r0, t0x, fma(r1, t1x, acc[ACS ? 0 : q].x));
+        acc[ACS ? 0 : q].y = fma(r0, t0y, fma(r1, t1y, acc[ACS ? 0 : q].y));
         rp[HOR ? 0 : q] = r1 * w;
       }
     }
@@ -422,7 +437,7 @@ far_pass2_kernel(FarArgs a) {
   for (int q = 0; q < NQ; ++q) {
     const int k = IRS ? kqs[q * NT + tid] : kq[IRS ? 0 : q];
     if (!k) continue;
-    double2 u = acc[q];
+    double2 u = ACS ? accs[q * NT] : acc[ACS ? 0 : q];
     if (HOR) {
       double post = 1.0;
       if (R.pr) post = ipow_f((double)k / a.Ld, R.pr);
@@ -931,13 +946,13 @@ static cudaError_t p1_d(const FarArgs& a, int n_units, cudaStream_t st) {
   return p1_t<N2, E, W, 1>(a, n_units, st);
 }
 
-template <int N1, int E, int MODE, int MINB>
+template <int N1, int E, int MODE, int MINB, bool ACS = false>
 static cudaError_t p2_t(const FarArgs& a, int gx, int gy, cudaStream_t st) {
   constexpr int T = N1 / E;
   constexpr int NCOL = MODE == 1 ? 1 : 2;
-  const int smem = (NCOL * (N1 + 4) + (TQS_ON(MODE, E, MINB) ? NCOL * E : 0)) * 16 +
+  const int smem = (NCOL * (N1 + 4) + (TQS_ON(MODE, E, MINB) ? NCOL * E : 0) + (ACS ? (E / 2) * NCOL * T : 0)) * 16 +
                    (IRS_K(E, MODE) ? (E / 2) * NCOL * T * 12 : 0);   // + IRS row factors, rows
-  auto k = far_pass2_kernel<N1, E, MODE, MINB>;
+  auto k = far_pass2_kernel<N1, E, MODE, MINB, ACS>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   note_launch(), k<<<dim3(gx, gy), NCOL * T, smem, st>>>(a);
@@ -964,8 +979,14 @@ static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
       case 2: return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : N1 >= 1024 ? 3 : 6)>(a, gx, gy, st);
       // case 3 (default): 512 columns at 5 CTAs/SM with step-table twiddles
       // (cfg2 far 70.8 -> 70.6 ms; 6 CTAs/SM 71.4)
-      case 3: if (N1 == 512) return p2_t<N1, 8, MODE, 5>(a, gx, gy, st);
-              if (N1 >= 1024) return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : 3)>(a, gx, gy, st);
+      // (bit 18 of the variant: accumulators in registers, the round-1 form)
+      case 3: if (g_far_variant & 0x40000) {
+                if (N1 == 512) return p2_t<N1, 8, MODE, 5>(a, gx, gy, st);
+                if (N1 >= 1024) return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : 3)>(a, gx, gy, st);
+              } else {
+                if (N1 == 512) return p2_t<N1, 8, MODE, 5, true>(a, gx, gy, st);
+                if (N1 >= 1024) return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : 3), true>(a, gx, gy, st);
+              }
               break;
       case 4: if (N1 == 512) return p2_t<N1, 8, MODE, 6>(a, gx, gy, st);
               if (N1 >= 1024) return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : 3)>(a, gx, gy, st);
