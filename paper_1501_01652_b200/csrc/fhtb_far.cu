@@ -1000,6 +1000,11 @@ static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
   constexpr int MINB = ((MODE == 0 || MODE == 3) && N1 == 2048) ? 2
                        : ((MODE == 0 || MODE == 3) && N1 == 1024) ? 3
                        : (MODE == 2 && N1 <= 1024) ? (N1 <= 512 ? 4 : 2) : 1;
+  // full blocks at 2048 points: accumulators in shared memory as for the narrow-column
+  // blocks (128 registers at 2 CTAs/SM spill otherwise; bit 19 of the variant: registers)
+  if constexpr ((MODE == 0 || MODE == 3) && N1 == 2048) {
+    if (!(g_far_variant & 0x80000)) return p2_t<N1, E, MODE, MINB, true>(a, gx, gy, st);
+  }
   return p2_t<N1, E, MODE, MINB>(a, gx, gy, st);
 }
 

@@ -184,6 +184,8 @@ struct DevCtx {
   JOrder* jtab = nullptr;          // orders 0..kMaxOrder
   unsigned long long* scratch = nullptr;
   int* nf = nullptr;               // set to 1 by any reduction that writes a non-finite output
+  double* stats = nullptr;         // fhtb_coef_stats output rows (grown on demand)
+  size_t stats_cap = 0;
   std::map<int, std::pair<double2*, double2*>> qtab;   // four-step twiddles per log2 Q
 };
 
@@ -791,11 +793,21 @@ int fhtb_coef_stats(const double* C, int64_t ldc, int32_t n_vec, int64_t n, int6
   if (n_vec == 0) return FHTB_OK;
   DevCtx* c;
   if (int r = get_ctx(&c)) return r;
-  double* d = nullptr;
-  CU(cudaMallocAsync((void**)&d, sizeof(double) * 3 * (size_t)n_vec, S(stream)));
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (c->stats_cap < (size_t)n_vec) {
+      CU(cudaDeviceSynchronize());
+      cudaFree(c->stats);
+      c->stats = nullptr;
+      c->stats_cap = 0;
+      const size_t cap = std::max<size_t>(256, 2 * (size_t)n_vec);
+      CU(cudaMalloc(&c->stats, sizeof(double) * 3 * cap));
+      c->stats_cap = cap;
+    }
+  }
+  double* d = c->stats;
   CU(launch_coef_stats(C, ldc, n_vec, n, n_split, b, nb, d, S(stream)));
   CU(cudaMemcpyAsync(out_host, d, sizeof(double) * 3 * (size_t)n_vec, cudaMemcpyDeviceToHost, S(stream)));
-  CU(cudaFreeAsync(d, S(stream)));
   CU(cudaStreamSynchronize(S(stream)));
   return FHTB_OK;
 }
@@ -934,7 +946,7 @@ int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
         if (ls <= 11 && ov <= 0) form = 1;
         else if (ls <= 11 && ov <= (1LL << ls) / 16) form = 2;
         else if (ls + 1 <= 11) { ls += 1; form = 1; }
-        else if (ls <= 12 && !was_rows) form = 0;
+        else if (ls <= 12) form = 0;
         if (form >= 0 && g->logQ - ls >= 4 && (1LL << ls) < g->L) {
           x.dmode = 3 + form;
           x.dlogL1 = g->logQ - ls;
