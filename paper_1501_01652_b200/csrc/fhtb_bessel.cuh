@@ -68,14 +68,18 @@ __device__ __forceinline__ double jn_hankel(double z, const JOrder& c) {
 }
 
 __device__ __forceinline__ int miller_start(double b) {
-  return (int)ceil(b + 10.0 + 11.0 * cbrt(b));
+  // b + 10 + 11 b^{1/3} (bessel.py:197-229), the cube root in single precision
+  // scaled up by more than its error (1 ulp + the rounding of b), so that the
+  // start order is never below the reference's and equals it except when
+  // the exact value lies within ~3e-7 relative of an integer
+  return (int)ceil(b + 10.0 + 11.0 * ((double)cbrtf((float)b) * (1.0 + 3e-7)));
 }
 
 // Miller for a single order nu, mid-range z > 0.
 __device__ __forceinline__ double jn_miller(int nu, double z) {
   const double b = fmax((double)nu, z);
   const int k0 = miller_start(b);
-  const double rz = 1.0 / z;
+  const double rz = __drcp_rn(z);          // = 1.0 / z, correctly rounded
   double up = 0.0, cur = 1e-30, nrm = 0.0, cap = 0.0;
   // orders above nu: two steps per trip, no capture, one overflow check
   int k = k0;
@@ -161,7 +165,7 @@ __device__ __forceinline__ void jn_all(int omax, double z, const JOrder* __restr
   const double b = fmax((double)omax, z);
   // start at least at OMAX so the capture phase below has static indices
   const int k0 = max(miller_start(b), OMAX);
-  const double rz = 1.0 / z;
+  const double rz = __drcp_rn(z);          // = 1.0 / z, correctly rounded
   double up = 0.0, cur = 1e-30, nrm = 0.0;
   // phase 1: k = k0 .. OMAX+1 produce f_{k-1} for orders >= OMAX (no capture);
   // two steps per trip (one even order), overflow check once per trip (the
@@ -247,7 +251,7 @@ __device__ __forceinline__ void jn_window(int omin, int omax, double z, const JO
   const int top = omin + W;                 // first order above the window
   const double b = fmax((double)omax, z);
   const int k0 = max(miller_start(b), top);
-  const double rz = 1.0 / z;
+  const double rz = __drcp_rn(z);          // = 1.0 / z, correctly rounded
   double up = 0.0, cur = 1e-30, nrm = 0.0;
   // phase 1: k = k0 .. top+1 produce f_{k-1} for orders >= top (no capture)
   for (int k = k0; k > top; --k) {
