@@ -257,6 +257,51 @@ int get_ctx(DevCtx** out) {
   return FHTB_OK;
 }
 
+// Per-call tables (requests, units, near-field groups) go to the device through a
+// ring of pinned staging slots: a cudaMemcpyAsync from pageable memory first
+// synchronises the stream, which stalls the host behind the previous
+// application and breaks the group pipeline of fhtb_apply_host.
+constexpr size_t kStageSlotBytes = 512 << 10;
+constexpr int kStageSlots = 32;
+struct StageRing {
+  char* base = nullptr;
+  cudaEvent_t ev[kStageSlots];
+  bool used[kStageSlots];
+  int next = 0;
+};
+std::map<int, StageRing> g_stage;
+
+cudaError_t h2d_tables(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return cudaSuccess;
+  if (bytes > kStageSlotBytes) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_mu);
+  StageRing& r = g_stage[dev];
+  if (!r.base) {
+    e = cudaMallocHost((void**)&r.base, kStageSlotBytes * kStageSlots);
+    if (e != cudaSuccess) { r.base = nullptr; return e; }
+    for (int i = 0; i < kStageSlots; ++i) {
+      e = cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+      r.used[i] = false;
+    }
+  }
+  const int i = r.next;
+  r.next = (r.next + 1) % kStageSlots;
+  if (r.used[i]) {
+    e = cudaEventSynchronize(r.ev[i]);         // the copy that last used this slot (long done)
+    if (e != cudaSuccess) return e;
+  }
+  char* slot = r.base + (size_t)i * kStageSlotBytes;
+  std::memcpy(slot, src, bytes);
+  e = cudaMemcpyAsync(dst, slot, bytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  r.used[i] = true;
+  return cudaEventRecord(r.ev[i], st);
+}
+
 // e^{+2 pi i m / Q} = qlo[m & (2^b - 1)] * qhi[m >> b],  b = min(12, log2 Q)
 int get_qtab(DevCtx* c, int logQ, double2** lo, double2** hi, int* bits) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -1514,8 +1559,8 @@ int run_exchange(const fhtb_grid* g, DevCtx* ctx, const std::vector<ReqDesc>& rs
   int2* d_xrow = cv.take<int2>(L2);
   double* part = cv.take<double>((size_t)std::min<long long>(U, n) * g->n_out);
   if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small (exchange mode)");
-  CU(cudaMemcpyAsync(d_units, units.data(), n * sizeof(UnitDesc), cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(d_xrow, xrow.data(), L2 * sizeof(int2), cudaMemcpyHostToDevice, st));
+  CU(h2d_tables(d_units, units.data(), n * sizeof(UnitDesc), st));
+  CU(h2d_tables(d_xrow, xrow.data(), L2 * sizeof(int2), st));
   FarArgs a;
   std::memset(&a, 0, sizeof a);
   a.L = g->L;
@@ -1683,7 +1728,7 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
 
   Carve cv{(char*)ws, ws_bytes};
   ReqDesc* d_req = cv.take<ReqDesc>(n_req);
-  if (!hp) CU(cudaMemcpyAsync(d_req, rs.data(), n_req * sizeof(ReqDesc), cudaMemcpyHostToDevice, st));
+  if (!hp) CU(h2d_tables(d_req, rs.data(), n_req * sizeof(ReqDesc), st));
 
   // Near field concurrently with the far field (both requested): it runs on
   // an auxiliary stream into a separate buffer Fn, added to F at the end on
@@ -1727,13 +1772,13 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
     ReqDesc* d_nreq = split ? cv.take<ReqDesc>(nreq.size()) : nullptr;
     double* part = g->n_slots ? cv.take<double>((size_t)g->n_slots * n_vec * kNearRT) : nullptr;
     if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small");
-    CU(cudaMemcpyAsync(d_q0, q0.data(), q0.size() * sizeof(int), cudaMemcpyHostToDevice, nst));
-    CU(cudaMemcpyAsync(d_v0, v0.data(), v0.size() * sizeof(int), cudaMemcpyHostToDevice, nst));
-    CU(cudaMemcpyAsync(d_vs, vstart.data(), vstart.size() * sizeof(int), cudaMemcpyHostToDevice, nst));
-    CU(cudaMemcpyAsync(d_vc, vcol.data(), vcol.size() * sizeof(int), cudaMemcpyHostToDevice, nst));
+    CU(h2d_tables(d_q0, q0.data(), q0.size() * sizeof(int), nst));
+    CU(h2d_tables(d_v0, v0.data(), v0.size() * sizeof(int), nst));
+    CU(h2d_tables(d_vs, vstart.data(), vstart.size() * sizeof(int), nst));
+    CU(h2d_tables(d_vc, vcol.data(), vcol.size() * sizeof(int), nst));
     if (split) {
-      CU(cudaMemcpyAsync(d_cls, cls.data(), cls.size() * sizeof(int2), cudaMemcpyHostToDevice, nst));
-      CU(cudaMemcpyAsync(d_nreq, nreq.data(), nreq.size() * sizeof(ReqDesc), cudaMemcpyHostToDevice, nst));
+      CU(h2d_tables(d_cls, cls.data(), cls.size() * sizeof(int2), nst));
+      CU(h2d_tables(d_nreq, nreq.data(), nreq.size() * sizeof(ReqDesc), nst));
     }
     NearArgs na;
     std::memset(&na, 0, sizeof na);
@@ -1809,10 +1854,10 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
         ts = pipe ? ax->cs[0] : st;
         CU(cudaStreamWaitEvent(ts, hp->ready, 0));
         if (hp->region_free) CU(cudaStreamWaitEvent(ts, hp->region_free, 0));
-        CU(cudaMemcpyAsync(d_req, rs.data(), n_req * sizeof(ReqDesc), cudaMemcpyHostToDevice, ts));
+        CU(h2d_tables(d_req, rs.data(), n_req * sizeof(ReqDesc), ts));
       }
-      CU(cudaMemcpyAsync(d_units, fp.units.data(), nu * sizeof(UnitDesc), cudaMemcpyHostToDevice, ts));
-      CU(cudaMemcpyAsync(d_ch, fp.chunks.data(), fp.chunks.size() * sizeof(int2), cudaMemcpyHostToDevice, ts));
+      CU(h2d_tables(d_units, fp.units.data(), nu * sizeof(UnitDesc), ts));
+      CU(h2d_tables(d_ch, fp.chunks.data(), fp.chunks.size() * sizeof(int2), ts));
       FarArgs a;
       std::memset(&a, 0, sizeof a);
       a.L = g->L;
@@ -2019,13 +2064,13 @@ int fhtb_direct_apply(const fhtb_direct_desc* d, const fhtb_request* reqs, int32
   int* d_vc = cv.take<int>(vcol.size());
   double* part = ns ? cv.take<double>((size_t)ns * n_vec * kNearRT) : nullptr;
   if (!cv.ok) return fail(FHTB_EINVAL, "workspace too small");
-  CU(cudaMemcpyAsync(d_req, rs.data(), n_req * sizeof(ReqDesc), cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(d_vs, vstart.data(), vstart.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(d_vc, vcol.data(), vcol.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-  if (!tiles.empty()) CU(cudaMemcpyAsync(d_tiles, tiles.data(), tiles.size() * sizeof(NearTile), cudaMemcpyHostToDevice, st));
-  if (!rts.empty()) CU(cudaMemcpyAsync(d_rts, rts.data(), rts.size() * sizeof(NearRowTile), cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(d_q0, q0.data(), q0.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(d_v0, v0.data(), v0.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  CU(h2d_tables(d_req, rs.data(), n_req * sizeof(ReqDesc), st));
+  CU(h2d_tables(d_vs, vstart.data(), vstart.size() * sizeof(int), st));
+  CU(h2d_tables(d_vc, vcol.data(), vcol.size() * sizeof(int), st));
+  if (!tiles.empty()) CU(h2d_tables(d_tiles, tiles.data(), tiles.size() * sizeof(NearTile), st));
+  if (!rts.empty()) CU(h2d_tables(d_rts, rts.data(), rts.size() * sizeof(NearRowTile), st));
+  CU(h2d_tables(d_q0, q0.data(), q0.size() * sizeof(int), st));
+  CU(h2d_tables(d_v0, v0.data(), v0.size() * sizeof(int), st));
   NearArgs na;
   std::memset(&na, 0, sizeof na);
   na.tiles = d_tiles;
