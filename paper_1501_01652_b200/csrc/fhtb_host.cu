@@ -1854,10 +1854,17 @@ int apply_impl(const fhtb_grid* g, const fhtb_request* reqs, int32_t n_req, cons
         ts = pipe ? ax->cs[0] : st;
         CU(cudaStreamWaitEvent(ts, hp->ready, 0));
         if (hp->region_free) CU(cudaStreamWaitEvent(ts, hp->region_free, 0));
-        CU(h2d_tables(d_req, rs.data(), n_req * sizeof(ReqDesc), ts));
+        // (host pipe: plain pageable copies.  Their implicit wait for the stream paces the
+        // host to one vector group ahead of the device; with the pinned ring the host
+        // enqueues all groups at once and the copy-in of later groups competes with the
+        // copy-out of earlier ones: e2e 871 -> 784 transforms/s on cfg2)
+        CU(cudaMemcpyAsync(d_req, rs.data(), n_req * sizeof(ReqDesc), cudaMemcpyHostToDevice, ts));
+        CU(cudaMemcpyAsync(d_units, fp.units.data(), nu * sizeof(UnitDesc), cudaMemcpyHostToDevice, ts));
+        CU(cudaMemcpyAsync(d_ch, fp.chunks.data(), fp.chunks.size() * sizeof(int2), cudaMemcpyHostToDevice, ts));
+      } else {
+        CU(h2d_tables(d_units, fp.units.data(), nu * sizeof(UnitDesc), ts));
+        CU(h2d_tables(d_ch, fp.chunks.data(), fp.chunks.size() * sizeof(int2), ts));
       }
-      CU(h2d_tables(d_units, fp.units.data(), nu * sizeof(UnitDesc), ts));
-      CU(h2d_tables(d_ch, fp.chunks.data(), fp.chunks.size() * sizeof(int2), ts));
       FarArgs a;
       std::memset(&a, 0, sizeof a);
       a.L = g->L;
