@@ -199,6 +199,28 @@ far_pass1p_kernel(FarArgs a) {
   }
 }
 
+// mbarrier / bulk-copy helpers (column tables of the narrow-column blocks)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// global -> shared bulk copy of `bytes` (multiple of 16, both 16-byte aligned), completion on `bar`
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // --------------------------------------------- pass 2 / one-pass epilogue
 //
 // MODE 0: two-pass, columns read from G.
@@ -228,7 +250,11 @@ far_pass1p_kernel(FarArgs a) {
 // at the register caps of these shapes (128 at 2048 points, 96 at 512) ncu counted
 // as many local (spill) loads and stores as global loads (variant bit 18 turns it off)
 // (template parameter ACS of the kernel)
-template <int N1, int E, int MODE, int MINB, bool ACS = false>
+// UBLT: template parameter (library option far_bulk_tables); measured on cfg2: far field
+// 63.95 -> 64.85 ms with the bulk-copied tables (the table hits in L1 either way; the
+// copy adds a shared-memory read per point to kernels bound by that pipe), so off
+#define UBL_ON(MODE, E, MINB, N1, ACS, UBLT) ((UBLT) && (ACS) && (MODE) == 2 && TQS_ON(MODE, E, MINB) && (N1) <= 1024)
+template <int N1, int E, int MODE, int MINB, bool ACS = false, bool UBLT = false>
 __global__ void __launch_bounds__((MODE == 1 ? 1 : 2) * (N1 / E), MINB)
 far_pass2_kernel(FarArgs a) {
   constexpr bool ONEPASS = (MODE == 1);
@@ -271,6 +297,11 @@ far_pass2_kernel(FarArgs a) {
   int* kqs = reinterpret_cast<int*>(irs + (IRS ? NQ * NT : 0));      // IRS: row indices too
   double ir[IRS ? 1 : NQ], rp[HOR ? 1 : NQ];
   constexpr bool ACSC = ACS, acs = ACS;
+  // UBL: the column table u_p of a narrow-column unit (N1 complex per pair, read by
+  // both columns of every CTA) arrives by bulk copy into a two-slot shared-memory
+  // buffer, pair p+1 while pair p is transformed (mbarrier per slot), instead of
+  // LDG.128 through L1 by both halves of the CTA
+  constexpr bool UBL = UBL_ON(MODE, E, MINB, N1, ACS, UBLT);
   double2* accs = reinterpret_cast<double2*>(kqs + (IRS ? NQ * NT : 0)) + tid;   // [q * NT]
   double2 acc[ACS ? 1 : NQ];
 #pragma unroll
@@ -321,11 +352,20 @@ far_pass2_kernel(FarArgs a) {
 #pragma unroll
     for (int e = 0; e < E; ++e) load_col(a, R, cA, cB, tt + T * e, v[ONEPASS ? e : 0], iw[ONEPASS ? e : 0]);
   }
+  double2* ub = reinterpret_cast<double2*>(accs - tid + (ACS ? NQ * NT : 0));        // [2][N1]
+  unsigned long long* ubar = reinterpret_cast<unsigned long long*>(ub + 2 * N1);   // [2]
   if (MODE == 2 && TQS) {
     double2* st = sm2 + NCOL * NP + h * E;
     if (tt < E) st[tt] = myk2 ? qtw(a, (long long)T * tt * myk2) : make_double2(1.0, 0.0);
     tb = myk2 ? qtw(a, (long long)tt * myk2) : make_double2(1.0, 0.0);
+    if (UBL && tid == 0) {
+      mbar_init(ubar, 1);
+      mbar_init(ubar + 1, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
+    if (UBL && tid == 0 && a.p1 > a.p0)
+      bulk_load(ub, a.G + (long long)(ul * a.M + (a.p1 - 1)) * N1, N1 * 16, ubar);
   } else if (MODE == 2) {
 #pragma unroll
     for (int e = 0; e < E; ++e)
@@ -351,6 +391,10 @@ far_pass2_kernel(FarArgs a) {
       }
     } else if (MODE == 2) {
       const double2* u = a.G + (long long)(ul * a.M + p) * N1;
+      if (UBL) {
+        while (!mbar_try_wait(ubar + (pi & 1), (pi >> 1) & 1)) {}
+        u = ub + (pi & 1) * N1;
+      }
       if (TQS) {
         const double2* st = sm2 + NCOL * NP + h * E;
 #pragma unroll
@@ -383,6 +427,11 @@ far_pass2_kernel(FarArgs a) {
       ac1 = R.ac[i1] * bisig, bc1 = R.bc[i1] * bisig;
     }
     __syncthreads();
+    if (UBL && tid == 0 && pi + 1 < a.p1 - a.p0) {
+      // every thread has read slot (pi+1)&1 (pair pi-1) before the barrier above
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bulk_load(ub + ((pi + 1) & 1) * N1, a.G + (long long)(ul * a.M + (p - 1)) * N1, N1 * 16, ubar + ((pi + 1) & 1));
+    }
     block_fft<N1, E, 1>(z, sm2 + h * NP, tt, tw);
     __syncthreads();
 #pragma unroll
@@ -864,6 +913,7 @@ __global__ void far_reduce_kernel(FarArgs a, int n_units) {
 // pass 2; 12-15: per-pair pass 1; bit 16: no TMA stores; 20-23: narrow-column
 // FFT shape.  Default = best measured on B200.
 int g_far_variant = 20 + (3 << 20);
+int g_far_bulk = 0;      // narrow-column tables by bulk copy (cp.async.bulk + mbarrier), see UBL_ON
 
 // 2D tensor map over G viewed as rows of 2*L1 doubles (one row per (unit,
 // pair, k2)); cuTensorMapEncodeTiled is fetched through the runtime so the
@@ -946,13 +996,14 @@ static cudaError_t p1_d(const FarArgs& a, int n_units, cudaStream_t st) {
   return p1_t<N2, E, W, 1>(a, n_units, st);
 }
 
-template <int N1, int E, int MODE, int MINB, bool ACS = false>
+template <int N1, int E, int MODE, int MINB, bool ACS = false, bool UBLT = false>
 static cudaError_t p2_t(const FarArgs& a, int gx, int gy, cudaStream_t st) {
   constexpr int T = N1 / E;
   constexpr int NCOL = MODE == 1 ? 1 : 2;
-  const int smem = (NCOL * (N1 + 4) + (TQS_ON(MODE, E, MINB) ? NCOL * E : 0) + (ACS ? (E / 2) * NCOL * T : 0)) * 16 +
+  const int smem = (NCOL * (N1 + 4) + (TQS_ON(MODE, E, MINB) ? NCOL * E : 0) + (ACS ? (E / 2) * NCOL * T : 0) +
+                    (UBL_ON(MODE, E, MINB, N1, ACS, UBLT) ? 2 * N1 + 1 : 0)) * 16 +
                    (IRS_K(E, MODE) ? (E / 2) * NCOL * T * 12 : 0);   // + IRS row factors, rows
-  auto k = far_pass2_kernel<N1, E, MODE, MINB, ACS>;
+  auto k = far_pass2_kernel<N1, E, MODE, MINB, ACS, UBLT>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   note_launch(), k<<<dim3(gx, gy), NCOL * T, smem, st>>>(a);
@@ -984,7 +1035,9 @@ static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
                 if (N1 == 512) return p2_t<N1, 8, MODE, 5>(a, gx, gy, st);
                 if (N1 >= 1024) return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : 3)>(a, gx, gy, st);
               } else {
+                if (N1 == 512 && g_far_bulk) return p2_t<N1, 8, MODE, 5, true, true>(a, gx, gy, st);
                 if (N1 == 512) return p2_t<N1, 8, MODE, 5, true>(a, gx, gy, st);
+                if (N1 == 1024 && g_far_bulk) return p2_t<N1, 16, MODE, 3, true, true>(a, gx, gy, st);
                 if (N1 >= 1024) return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : 3), true>(a, gx, gy, st);
               }
               break;
