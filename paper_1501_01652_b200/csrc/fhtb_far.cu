@@ -1048,7 +1048,11 @@ static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
     }
   }
   // 256-point narrow-column blocks (far_min_cols = 8): 64-thread CTAs, 10 per SM
-  if constexpr (MODE == 2 && N1 == 256) return p2_t<N1, 8, MODE, 10, true>(a, gx, gy, st);
+  if constexpr (MODE == 2 && N1 == 256) {
+    // 16 points per thread: two radix-16 passes, one exchange, one-warp CTAs (cfg2 far field
+    // with the 91-column block at 256 points: 63.9 ms with 8 points per thread, 63.5 with 16)
+    return p2_t<N1, 16, MODE, 16, true>(a, gx, gy, st);
+  }
   // narrow-column blocks carry a complex state per element: 8 points/thread
   constexpr int E = MODE == 2 ? (N1 >= 8 ? 8 : N1) : (N1 >= 16 ? 16 : N1);
   // two columns of 2048 with E = 16: 256 threads, 2 CTAs/SM measured best

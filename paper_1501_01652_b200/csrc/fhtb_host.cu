@@ -41,7 +41,7 @@ int g_prune_rows = 11;                     // narrow-row blocks: rows below 2^g_
 int g_rowsum = 2;                          // narrow-row blocks: fully fused forms (dmode 3..5); 1: only blocks that would run both passes; 0: off
 int g_rowsum_min_m = 4;                    // ... for blocks already pruned to row sums: only with at least this many pairs
 int g_rowdot_bins = 1;                     // narrow-row blocks: at most this many pass-2 bins per column
-int g_min_lc = 9;                          // narrow-column blocks: smallest column FFT 2^g_min_lc
+int g_min_lc = 0;                          // narrow-column blocks: smallest column FFT 2^g_min_lc (0: 256 points from 8 pairs on, else 512)
 int g_near_priority = 0;                   // near-field stream priority (see get_aux)
 int g_far_prefetch = 1;                    // L2 prefetch of the coefficient rows before pass 1
 int g_host_taper = 4;                      // fhtb_apply_host: inner/outer group size ratio
@@ -715,7 +715,7 @@ int fhtb_set_option(const char* key, int64_t value) {
     return FHTB_OK;
   }
   if (!std::strcmp(key, "far_min_cols")) {
-    if (value < 7 || value > 12) return fail(FHTB_EINVAL, "far_min_cols must be 7..12");
+    if (value != 0 && (value < 7 || value > 12)) return fail(FHTB_EINVAL, "far_min_cols must be 0 (auto) or 7..12");
     g_min_lc = (int)value;
     return FHTB_OK;
   }
@@ -957,7 +957,10 @@ int fhtb_grid_create(const fhtb_grid_desc* d, fhtb_grid** out) {
       x.dlogL1 = g->logN1;
       const long long cend = std::min(x.c1, g->n_data_cols + 1);   // columns n < cend
       // narrow-column blocks are shifted to their first column (fhtb_far.cu MODE 2)
-      const int lc = std::max(g_min_lc, ilog2ll(std::max<long long>(cend - x.c0, 2)));
+      // smallest column FFT: 256 points (two radix-16 passes, one-warp CTAs) pay from 8 pairs on
+      // (cfg2 1e-15 far 64.0 -> 63.5 ms, FB cfg3 +1.5%; with 3 / 5 pairs -1.3% / -0.8%)
+      const int min_lc = g_min_lc ? g_min_lc : (g->M >= 8 ? 8 : 9);
+      const int lc = std::max(min_lc, ilog2ll(std::max<long long>(cend - x.c0, 2)));
       // L2 >= r1 so that every block row has k1 = 0; keep L2 >= 1024 (the
       // pass-1 FFT is least efficient below that) and L1 <= 2048 (rowdot sums)
       const int lr = std::max(std::max(g->logQ - 11, 10), ilog2ll(std::max<long long>(x.r1, 2)));

@@ -18,7 +18,7 @@ from paper_1501_01652_b200.schlomilch import _grid_cache, _grid_lock
 
 pytestmark = pytest.mark.gpu
 
-DEFAULTS = {b"far_rowdot_bins": 1, b"far_min_cols": 9, b"near_chunk_cols": 8192,
+DEFAULTS = {b"far_rowdot_bins": 1, b"far_min_cols": 0, b"near_chunk_cols": 8192,
             b"near_chunk_cols_multi": 1024, b"far_prefetch": 1, b"near_priority": 0, b"far_prune_rows": 11, b"far_rowsum": 2, b"far_bulk_tables": 0}
 
 
