@@ -176,3 +176,32 @@ def test_dht_largest_grids_vs_direct_rows(cuda_dev, lg, eps):
     _direct_apply(scale, r_dev, n, [0], [dict(vec=0, terms=[(0, 1.0)])], C, ref)
     err = float((F[0, k - 1] - ref[0]).abs().max())
     assert err <= 10 * eps * float(C.abs().sum()), err
+
+
+@pytest.mark.parametrize("n", [2 ** 13, 2 ** 14, 12000])
+@pytest.mark.parametrize("eps", [1e-3, 1e-8, 1e-15])
+def test_all_tasks_vs_direct_summation_up_to_2_14(cuda_dev, n, eps):
+    """North star: all three tasks against direct O(N^2) fp64 summation for
+    N <= 2^14 at every eps (whole output vectors; the direct sums are the
+    library's schlomilch_direct / fourier_bessel_direct / dht_direct, pinned to
+    the reference's direct sums by the golden fixtures).  N = 2^13 and 2^14
+    are the smallest two-pass grids (few columns per fused narrow-row unit),
+    12000 runs the chirp-z far field."""
+    rng = np.random.default_rng([41, n])
+    c = rng.standard_normal(n) / np.arange(1, n + 1)
+    tol = 10 * eps * np.abs(c).sum()
+    for nu, gamma in ((0, 0.0), (4, 4.0)):
+        f = fh.schlomilch_fast(fh.select_params(nu, n, eps, gamma=gamma), c)
+        d = fh.schlomilch_direct(nu, gamma, c)
+        assert np.max(np.abs(f - d)) <= tol, ("schlomilch", nu, n, eps, np.max(np.abs(f - d)), tol)
+    if n <= 2 ** 13:
+        cu = rng.uniform(-1, 1, n)
+        roots = fh.bessel_roots_j0(n)
+        f = fh.fourier_bessel_eval(0, cu, eps, roots=roots)
+        d = fh.fourier_bessel_direct(0, cu, roots=roots)
+        assert np.max(np.abs(f - d)) <= 10 * eps * np.abs(cu).sum(), ("fb", n, eps)
+        plan = fh.dht_plan(n, eps)
+        cn = rng.standard_normal(n)
+        f = fh.dht(plan, cn)
+        d = fh.dht_direct(plan, cn)
+        assert np.max(np.abs(f - d)) <= 10 * eps * np.abs(cn).sum(), ("dht", n, eps)
