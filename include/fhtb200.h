@@ -73,6 +73,11 @@ int fhtb_kernel_times(double* ms, double* bytes, double* flops, int64_t* launche
  * fourier_bessel.py:208-225 and dht.py:140-157 (norm1, b_max, nonzero). */
 int fhtb_coef_stats(const double* C, int64_t ldc, int32_t n_vec, int64_t n, int64_t n_split, const double* b,
                     int64_t nb, double* out_host, void* stream);
+/* out[v][i] = alpha * a[v][i] * w[i] (w may be null), and max_i |alpha a[i] - b[i]| returned to
+ * the host: the diagonal scalings and the residual of dht_self_inverse_residual (dht.py:179-194). */
+int fhtb_mul_rows(double* out, int64_t ldo, const double* a, int64_t lda, const double* w, double alpha, int64_t n,
+                  int32_t n_vec, void* stream);
+int fhtb_max_abs_diff(const double* a, double alpha, const double* b, int64_t n, double* out_host, void* stream);
 /* F[v][0..n) = 0 for v < n_vec (stream-ordered memset of result rows). */
 int fhtb_zero_rows(double* F, int64_t ldf, int32_t n_vec, int64_t n, void* stream);
 /* out[i] = J_nu(z[i]); replaces bessel.py:232-260 (bessel_j, array path). */

@@ -53,6 +53,8 @@ EXPORTS = {
     "fhtb_nonfinite_check": (i32, [vp]),
     "fhtb_coef_stats": (i32, [vp, i64, i32, i64, i64, vp, i64, P_f64, vp]),
     "fhtb_zero_rows": (i32, [vp, i64, i32, i64, vp]),
+    "fhtb_mul_rows": (i32, [vp, i64, vp, i64, vp, f64, i64, i32, vp]),
+    "fhtb_max_abs_diff": (i32, [vp, f64, vp, i64, P_f64, vp]),
     "fhtb_init": (i32, []),
     "fhtb_set_option": (i32, [ctypes.c_char_p, i64]),
     "fhtb_kernel_families": (i32, []),

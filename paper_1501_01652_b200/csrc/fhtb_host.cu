@@ -861,6 +861,26 @@ int fhtb_coef_stats(const double* C, int64_t ldc, int32_t n_vec, int64_t n, int6
   return FHTB_OK;
 }
 
+int fhtb_mul_rows(double* out, int64_t ldo, const double* a, int64_t lda, const double* w, double alpha, int64_t n,
+                  int32_t n_vec, void* stream) {
+  if (n < 0 || n_vec < 0 || ldo < n || lda < n) return fail(FHTB_EINVAL, "bad mul_rows arguments");
+  CU(launch_mul_rows(out, ldo, a, lda, w, alpha, n, n_vec, S(stream)));
+  return FHTB_OK;
+}
+
+int fhtb_max_abs_diff(const double* a, double alpha, const double* b, int64_t n, double* out_host, void* stream) {
+  if (n < 0 || !out_host) return fail(FHTB_EINVAL, "bad max_abs_diff arguments");
+  DevCtx* c;
+  if (int r = get_ctx(&c)) return r;
+  CU(cudaMemsetAsync(c->scratch, 0, 8, S(stream)));
+  CU(launch_max_abs_diff(a, alpha, b, n, c->scratch, S(stream)));
+  unsigned long long bits = 0;
+  CU(cudaMemcpyAsync(&bits, c->scratch, 8, cudaMemcpyDeviceToHost, S(stream)));
+  CU(cudaStreamSynchronize(S(stream)));
+  std::memcpy(out_host, &bits, 8);
+  return FHTB_OK;
+}
+
 int fhtb_zero_rows(double* F, int64_t ldf, int32_t n_vec, int64_t n, void* stream) {
   if (n_vec < 0 || n < 0 || ldf < n) return fail(FHTB_EINVAL, "bad zero_rows arguments");
   if (n_vec == 0 || n == 0) return FHTB_OK;

@@ -145,6 +145,10 @@ cudaError_t launch_taylor_eval(int nu, int n_terms, double inv_fact, const doubl
                                double* out, cudaStream_t st);
 cudaError_t launch_coef_stats(const double* C, long long ldc, int n_vec, long long n, long long n_split,
                               const double* b, long long nb, double* out, cudaStream_t st);
+cudaError_t launch_mul_rows(double* out, long long ldo, const double* a, long long lda, const double* w, double alpha,
+                            long long n, int n_vec, cudaStream_t st);
+cudaError_t launch_max_abs_diff(const double* a, double alpha, const double* b, long long n, unsigned long long* res,
+                                cudaStream_t st);
 cudaError_t launch_roots_j0(const JOrder* tab, long long count, double* roots, double* pert,
                             unsigned long long* resid_bits, cudaStream_t st);
 cudaError_t launch_fft_batch(int logN, int sign, const double2* in, double2* out, long long batch,

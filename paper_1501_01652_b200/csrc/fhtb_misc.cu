@@ -216,6 +216,41 @@ cudaError_t launch_coef_stats(const double* C, long long ldc, int n_vec, long lo
   return cudaGetLastError();
 }
 
+// out[v][i] = alpha * a[v][i] * w[i]  (dht.py:188-190: the diagonal D_v of the self-inverse check)
+__global__ void mul_rows_kernel(double* __restrict__ out, long long ldo, const double* __restrict__ a, long long lda,
+                                const double* __restrict__ w, double alpha, long long n, int n_vec) {
+  const long long tot = n * n_vec;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const long long v = e / n, i = e % n;
+    out[v * ldo + i] = alpha * a[v * lda + i] * (w ? w[i] : 1.0);
+  }
+}
+
+cudaError_t launch_mul_rows(double* out, long long ldo, const double* a, long long lda, const double* w, double alpha,
+                            long long n, int n_vec, cudaStream_t st) {
+  if (n * n_vec == 0) return cudaSuccess;
+  note_launch(), mul_rows_kernel<<<grid_for(n * n_vec, 256), 256, 0, st>>>(out, ldo, a, lda, w, alpha, n, n_vec);
+  return cudaGetLastError();
+}
+
+// res[0] = max_i |alpha * a[i] - b[i]|  (bit pattern of a non-negative double, atomicMax)
+__global__ void max_abs_diff_kernel(const double* __restrict__ a, double alpha, const double* __restrict__ b,
+                                    long long n, unsigned long long* res) {
+  double m = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(alpha * a[i] - b[i]));
+#pragma unroll
+  for (int off = 16; off; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(res, (unsigned long long)__double_as_longlong(m));
+}
+
+cudaError_t launch_max_abs_diff(const double* a, double alpha, const double* b, long long n, unsigned long long* res,
+                                cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  note_launch(), max_abs_diff_kernel<<<grid_for(n, 256), 256, 0, st>>>(a, alpha, b, n, res);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_twiddles(double2* pool, int max_log, cudaStream_t st) {
   const long long total = (1LL << (max_log + 1)) - 2;
   note_launch(), twiddle_kernel<<<grid_for(total, 256), 256, 0, st>>>(pool, max_log);

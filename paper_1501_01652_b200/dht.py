@@ -12,6 +12,7 @@ reference's padding by 3N+3 zeros and its 4x redundant rows are never
 materialised.  Rows k <= row_split are summed directly (dht.py:175).
 """
 
+import ctypes
 import math
 from dataclasses import dataclass, field
 
@@ -163,7 +164,23 @@ def dht_self_inverse_residual(n, eps, c, method="fast", plan=None):
     if plan is None:
         plan = dht_plan(n, eps)
     apply_fn = dht if method == "fast" else dht_direct
-    y = apply_fn(plan, plan.weights * c)
-    y = apply_fn(plan, plan.weights * y)
-    c_round = y / plan.roots.roots[n] ** 2
-    return float(np.max(np.abs(c_round - c)))
+    if np.iscomplexobj(c) or c.ndim != 1:
+        y = apply_fn(plan, plan.weights * c)
+        y = apply_fn(plan, plan.weights * y)
+        return float(np.max(np.abs(y / plan.roots.roots[n] ** 2 - c)))
+    # the N-length scalings and the residual run in the library (device-resident throughout)
+    C = _device.to_dev_f64(c).reshape(1, -1)
+    w = plan.__dict__.get("_w_dev")
+    if w is None or w.device != C.device:
+        w = _device.to_dev_f64(plan.weights)
+        object.__setattr__(plan, "_w_dev", w)
+    t = torch.empty_like(C)
+    for src in (C, None):
+        a = C if src is not None else y
+        _lib.call("fhtb_mul_rows", _device.ptr(t), t.stride(0), _device.ptr(a), a.stride(0), _device.ptr(w), 1.0,
+                  n, 1, _device.stream_ptr())
+        y = apply_fn(plan, t)
+    res = ctypes.c_double(0.0)
+    _lib.call("fhtb_max_abs_diff", _device.ptr(y), 1.0 / float(plan.roots.roots[n]) ** 2, _device.ptr(C), n,
+              ctypes.byref(res), _device.stream_ptr())
+    return float(res.value)

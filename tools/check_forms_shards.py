@@ -1,3 +1,8 @@
+"""Far-field formulations against each other at large N: the default (fused narrow rows) and
+far_rowsum=0 results, and the 8-way pair split against the one-GPU result, at N = 2^22 and 2^24.
+
+    python tools/check_forms_shards.py
+"""
 import sys, os
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
