@@ -114,7 +114,7 @@ def load(path=LIB_PATH):
                              ("FHTB_NEAR_CHUNK_COLS_MULTI", b"near_chunk_cols_multi"), ("FHTB_NEAR_SPLIT", b"near_split"), ("FHTB_FAR_STREAMS", b"far_streams"),
                              ("FHTB_NEAR_OVERLAP", b"near_overlap"),
                              ("FHTB_FAR_PRUNE_ROWS", b"far_prune_rows"), ("FHTB_FAR_MIN_COLS", b"far_min_cols"),
-                             ("FHTB_FAR_ROWDOT_BINS", b"far_rowdot_bins"), ("FHTB_FAR_ROWSUM", b"far_rowsum"), ("FHTB_FAR_BULK_TABLES", b"far_bulk_tables"), ("FHTB_FAR_ROWSUM_MIN_PAIRS", b"far_rowsum_min_pairs"), ("FHTB_HOST_TAPER", b"host_taper"),
+                             ("FHTB_FAR_ROWDOT_BINS", b"far_rowdot_bins"), ("FHTB_FAR_ROWSUM", b"far_rowsum"), ("FHTB_FAR_BULK_TABLES", b"far_bulk_tables"), ("FHTB_FAR_HALF_PAIRING", b"far_half_pairing"), ("FHTB_FAR_ROWSUM_MIN_PAIRS", b"far_rowsum_min_pairs"), ("FHTB_HOST_TAPER", b"host_taper"),
                              ("FHTB_FAR_PREFETCH", b"far_prefetch"), ("FHTB_NEAR_PRIORITY", b"near_priority")):
                 if os.environ.get(env):
                     lib.fhtb_set_option(key, int(os.environ[env]))

@@ -254,7 +254,13 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
 // 63.95 -> 64.85 ms with the bulk-copied tables (the table hits in L1 either way; the
 // copy adds a shared-memory read per point to kernels bound by that pipe), so off
 #define UBL_ON(MODE, E, MINB, N1, ACS, UBLT) ((UBLT) && (ACS) && (MODE) == 2 && TQS_ON(MODE, E, MINB) && (N1) <= 1024)
-template <int N1, int E, int MODE, int MINB, bool ACS = false, bool UBLT = false>
+// HP (half pairing): every thread finishes the rows of its OWN lower-half FFT outputs
+// (k1 < N1/2, i.e. k = k2 + L2 k1 < L) straight from its registers; only the upper-half
+// outputs go through shared memory, once, as the partners conj Z[2L-k] = conj Z_b[N1-1-k1] of
+// the other column's rows: 8 + 8 bytes of shared-memory traffic per point for the
+// Z[k] / Z[2L-k] pairing instead of 16 + 16.  The CTA of column 0 (its own partner, plus row
+// L) keeps the general form: HP kernels cover the column pairs k2a >= 1.
+template <int N1, int E, int MODE, int MINB, bool ACS = false, bool UBLT = false, bool HP = false>
 __global__ void __launch_bounds__((MODE == 1 ? 1 : 2) * (N1 / E), MINB)
 far_pass2_kernel(FarArgs a) {
   constexpr bool ONEPASS = (MODE == 1);
@@ -271,7 +277,7 @@ far_pass2_kernel(FarArgs a) {
   const int tid = threadIdx.x, h = tid / T, tt = tid % T;
   const int L = (int)a.L;
   const int L2 = a.L2;
-  const int k2a = XCH ? a.xc0 + (int)blockIdx.x : (int)blockIdx.x, k2b = (L2 - k2a) % L2;
+  const int k2a = (XCH ? a.xc0 + (int)blockIdx.x : (int)blockIdx.x) + (HP ? 1 : 0), k2b = (L2 - k2a) % L2;
   const bool selfp = (k2a == k2b);
   const int myk2 = h == 0 ? k2a : k2b;
   const int ul = blockIdx.y;
@@ -287,7 +293,8 @@ far_pass2_kernel(FarArgs a) {
 
   // E <= 8: the shared-memory offsets of Z[k] and Z[2L-k] are kept per slot
   // (registers allow it); E = 16 recomputes them per pair
-  constexpr bool PRE = (E <= 8 && N1 >= 1024);
+  constexpr bool PRE = (E <= 8 && N1 >= 1024) && !HP;
+  constexpr int RLH = FftShape<N1, E>::RL / 2 > 0 ? FftShape<N1, E>::RL / 2 : 1;   // HP: lower-half slots per radix group
   int kq[IRS_K(E, MODE) ? 1 : NQ], oz[PRE ? NQ : 1], op[PRE ? NQ : 1];
   // IRS (E = 16, Horner modes): the row factors L/k live in shared memory
   // ([q][tid] after the FFT buffers) instead of NQ registers, which the
@@ -309,7 +316,14 @@ far_pass2_kernel(FarArgs a) {
     const int o = tid + NT * q;
     const int hh = o / HALF, qq = o % HALF;
     int k = 0;
-    if (hh < NCOL && !(selfp && hh == 1)) {
+    if (HP) {
+      // row of this thread's q-th lower-half output slot
+      const int s = (q / RLH) * (2 * RLH) + (q % RLH);
+      if (!(selfp && h == 1)) {
+        k = myk2 + L2 * fft_out_index<N1, E>(tt, s);
+        if (k < 1 || k > L || k < B.r0 || k >= B.r1) k = 0;
+      }
+    } else if (hh < NCOL && !(selfp && hh == 1)) {
       const int k2 = hh == 0 ? k2a : k2b;
       const int k1 = (k2 == 0) ? qq + 1 : qq;
       k = k2 + L2 * k1;
@@ -434,8 +448,15 @@ far_pass2_kernel(FarArgs a) {
     }
     block_fft<N1, E, 1>(z, sm2 + h * NP, tt, tw);
     __syncthreads();
+    if (HP) {
+      // upper-half outputs Z[k1 >= N1/2] of this column at index k1 - N1/2
 #pragma unroll
-    for (int s = 0; s < E; ++s) sm2[h * NP + swz<LOGE>(fft_out_index<N1, E>(tt, s))] = z[s];
+      for (int s = 0; s < E; ++s)
+        if ((s % (2 * RLH)) >= RLH) sm2[h * NP + fft_out_index<N1, E>(tt, s) - HALF] = z[s];
+    } else {
+#pragma unroll
+      for (int s = 0; s < E; ++s) sm2[h * NP + swz<LOGE>(fft_out_index<N1, E>(tt, s))] = z[s];
+    }
     __syncthreads();
     if (E > 8) {
       ac0 = R.ac[i0], bc0 = R.bc[i0];
@@ -446,8 +467,16 @@ far_pass2_kernel(FarArgs a) {
       const int k = IRS ? kqs[q * NT + tid] : kq[IRS ? 0 : q];
       if (!k) continue;
       const int kp = 2 * L - k;
-      const double2 Zk = sm2[PRE ? oz[PRE ? q : 0] : (((k & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(k >> lgL2)];
-      const double2 Zp = cconj(sm2[PRE ? op[PRE ? q : 0] : (((kp & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(kp >> lgL2)]);
+      double2 Zk, Zp;
+      if (HP) {
+        // own register; partner Z_b[N1 - 1 - k1] from the other column (this one if self-paired)
+        const int s = (q / RLH) * (2 * RLH) + (q % RLH);
+        Zk = z[s];
+        Zp = cconj(sm2[(selfp ? h : 1 - h) * NP + (HALF - 1 - fft_out_index<N1, E>(tt, s))]);
+      } else {
+        Zk = sm2[PRE ? oz[PRE ? q : 0] : (((k & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(k >> lgL2)];
+        Zp = cconj(sm2[PRE ? op[PRE ? q : 0] : (((kp & (L2 - 1)) == k2a) ? 0 : NP) + swz<LOGE>(kp >> lgL2)]);
+      }
       // 2 Ya, 2 Yb (the factor 1/2 is folded into r_0)
       double2 Ya = make_double2(Zk.x + Zp.x, Zk.y + Zp.y);
       double2 Yb = make_double2(Zk.y - Zp.y, Zp.x - Zk.x);
@@ -914,6 +943,7 @@ __global__ void far_reduce_kernel(FarArgs a, int n_units) {
 // FFT shape.  Default = best measured on B200.
 int g_far_variant = 20 + (3 << 20);
 int g_far_bulk = 0;      // narrow-column tables by bulk copy (cp.async.bulk + mbarrier), see UBL_ON
+int g_far_hp = 1;        // pass 2: half pairing (HP kernels) for the column pairs k2a >= 1
 
 // 2D tensor map over G viewed as rows of 2*L1 doubles (one row per (unit,
 // pair, k2)); cuTensorMapEncodeTiled is fetched through the runtime so the
@@ -996,13 +1026,25 @@ static cudaError_t p1_d(const FarArgs& a, int n_units, cudaStream_t st) {
   return p1_t<N2, E, W, 1>(a, n_units, st);
 }
 
-template <int N1, int E, int MODE, int MINB, bool ACS = false, bool UBLT = false>
+template <int N1, int E, int MODE, int MINB, bool ACS = false, bool UBLT = false, bool HP = false>
 static cudaError_t p2_t(const FarArgs& a, int gx, int gy, cudaStream_t st) {
   constexpr int T = N1 / E;
   constexpr int NCOL = MODE == 1 ? 1 : 2;
   const int smem = (NCOL * (N1 + 4) + (TQS_ON(MODE, E, MINB) ? NCOL * E : 0) + (ACS ? (E / 2) * NCOL * T : 0) +
                     (UBL_ON(MODE, E, MINB, N1, ACS, UBLT) ? 2 * N1 + 1 : 0)) * 16 +
                    (IRS_K(E, MODE) ? (E / 2) * NCOL * T * 12 : 0);   // + IRS row factors, rows
+  if constexpr (HP) {
+    // column pairs k2a >= 1 by the half-pairing kernel, column 0 by the general one
+    if (gx > 1) {
+      auto kh = far_pass2_kernel<N1, E, MODE, MINB, ACS, UBLT, true>;
+      cudaError_t eh = cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (eh != cudaSuccess) return eh;
+      note_launch(), kh<<<dim3(gx - 1, gy), NCOL * T, smem, st>>>(a);
+      eh = cudaGetLastError();
+      if (eh != cudaSuccess) return eh;
+    }
+    gx = 1;
+  }
   auto k = far_pass2_kernel<N1, E, MODE, MINB, ACS, UBLT>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -1036,8 +1078,10 @@ static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
                 if (N1 >= 1024) return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : 3)>(a, gx, gy, st);
               } else {
                 if (N1 == 512 && g_far_bulk) return p2_t<N1, 8, MODE, 5, true, true>(a, gx, gy, st);
+                if (N1 == 512 && g_far_hp) return p2_t<N1, 8, MODE, 5, true, false, true>(a, gx, gy, st);
                 if (N1 == 512) return p2_t<N1, 8, MODE, 5, true>(a, gx, gy, st);
                 if (N1 == 1024 && g_far_bulk) return p2_t<N1, 16, MODE, 3, true, true>(a, gx, gy, st);
+                if (N1 >= 1024 && g_far_hp) return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : 3), true, false, true>(a, gx, gy, st);
                 if (N1 >= 1024) return p2_t<N1, 16, MODE, (N1 >= 2048 ? 2 : 3), true>(a, gx, gy, st);
               }
               break;
@@ -1051,6 +1095,7 @@ static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
   if constexpr (MODE == 2 && N1 == 256) {
     // 16 points per thread: two radix-16 passes, one exchange, one-warp CTAs (cfg2 far field
     // with the 91-column block at 256 points: 63.9 ms with 8 points per thread, 63.5 with 16)
+    if (g_far_hp) return p2_t<N1, 16, MODE, 16, true, false, true>(a, gx, gy, st);
     return p2_t<N1, 16, MODE, 16, true>(a, gx, gy, st);
   }
   // narrow-column blocks carry a complex state per element: 8 points/thread
@@ -1062,6 +1107,7 @@ static cudaError_t p2_d(const FarArgs& a, int gx, int gy, cudaStream_t st) {
   // full blocks at 2048 points: accumulators in shared memory as for the narrow-column
   // blocks (128 registers at 2 CTAs/SM spill otherwise; bit 19 of the variant: registers)
   if constexpr ((MODE == 0 || MODE == 3) && N1 == 2048) {
+    if (!(g_far_variant & 0x80000) && MODE == 0 && g_far_hp) return p2_t<N1, E, MODE, MINB, true, false, true>(a, gx, gy, st);
     if (!(g_far_variant & 0x80000)) return p2_t<N1, E, MODE, MINB, true>(a, gx, gy, st);
   }
   return p2_t<N1, E, MODE, MINB>(a, gx, gy, st);

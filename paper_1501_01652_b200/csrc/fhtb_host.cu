@@ -741,6 +741,10 @@ int fhtb_set_option(const char* key, int64_t value) {
     g_chirp_variant = (int)value;
     return FHTB_OK;
   }
+  if (!std::strcmp(key, "far_half_pairing")) {
+    g_far_hp = value ? 1 : 0;
+    return FHTB_OK;
+  }
   if (!std::strcmp(key, "far_bulk_tables")) {
     g_far_bulk = value ? 1 : 0;
     return FHTB_OK;

@@ -91,6 +91,7 @@ cudaError_t launch_col_tables(double* w0, double* iw, long long L, double gamma,
 
 extern int g_far_variant;         // tuning knob for the hot far-field sizes
 extern int g_far_bulk;            // narrow-column tables by bulk copy into shared memory
+extern int g_far_hp;              // pass 2 half pairing
 extern int g_chirp_variant;       // tuning knob for the chirp-z passes
 
 cudaError_t launch_near(const NearArgs& a, int n_tiles, int n_groups, int max_cols, cudaStream_t st);

@@ -19,7 +19,7 @@ from paper_1501_01652_b200.schlomilch import _grid_cache, _grid_lock
 pytestmark = pytest.mark.gpu
 
 DEFAULTS = {b"far_rowdot_bins": 1, b"far_min_cols": 0, b"near_chunk_cols": 8192,
-            b"near_chunk_cols_multi": 1024, b"far_prefetch": 1, b"near_priority": 0, b"far_prune_rows": 11, b"far_rowsum": 2, b"far_bulk_tables": 0}
+            b"near_chunk_cols_multi": 1024, b"far_prefetch": 1, b"near_priority": 0, b"far_prune_rows": 11, b"far_rowsum": 2, b"far_bulk_tables": 0, b"far_half_pairing": 1}
 
 
 def _set(opts):
@@ -53,7 +53,7 @@ def _schl(n, nu, gamma, eps, batch, seed):
     ({b"far_rowsum": 0}, 2 ** 15), ({b"far_rowsum": 0}, 2 ** 22),
     ({b"far_rowsum": 0, b"far_rowdot_bins": 2}, 2 ** 19), ({b"far_rowsum": 0, b"far_rowdot_bins": 4}, 2 ** 20),
     ({b"far_rowsum": 0, b"far_prune_rows": 12}, 2 ** 20),
-    ({b"far_bulk_tables": 1}, 2 ** 20), ({b"far_min_cols": 7}, 2 ** 17), ({b"far_min_cols": 12}, 2 ** 17), ({b"far_prefetch": 0}, 2 ** 17),
+    ({b"far_bulk_tables": 1}, 2 ** 20), ({b"far_half_pairing": 0}, 2 ** 20), ({b"far_half_pairing": 0}, 2 ** 16), ({b"far_min_cols": 7}, 2 ** 17), ({b"far_min_cols": 12}, 2 ** 17), ({b"far_prefetch": 0}, 2 ** 17),
     ({b"near_chunk_cols": 512}, 2 ** 17),
 ])
 def test_far_forms_agree(cuda_dev, restore, opts, n):
@@ -68,7 +68,7 @@ def test_far_forms_agree(cuda_dev, restore, opts, n):
     assert bool((err <= tol).all()), (opts, err.cpu().numpy(), tol.cpu().numpy())
     # the option did take effect: a different formulation rounds differently,
     # a schedule-only option (prefetch) leaves the bits alone
-    if b"far_prefetch" in opts or b"far_bulk_tables" in opts:
+    if b"far_prefetch" in opts or b"far_bulk_tables" in opts or b"far_half_pairing" in opts:
         assert torch.equal(got, ref)
     else:
         assert not torch.equal(got, ref), opts
