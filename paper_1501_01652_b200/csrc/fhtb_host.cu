@@ -193,6 +193,7 @@ constexpr int kQBits = 12;
 inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
 
 std::mutex g_mu;
+std::mutex g_scratch_mu;            // serialises the users of DevCtx::scratch
 std::map<int, DevCtx> g_ctx;
 
 // Two auxiliary streams + events per (device, caller stream): far-field
@@ -821,6 +822,7 @@ int fhtb_roots_j0(int64_t count, double* roots, double* perturb, double* resid_m
   if (count < 1) return fail(FHTB_EINVAL, "count must be >= 1");
   DevCtx* c;
   if (int r = get_ctx(&c)) return r;
+  std::lock_guard<std::mutex> scratch_lk(g_scratch_mu);      // c->scratch is shared
   CU(cudaMemsetAsync(c->scratch, 0, 16, S(stream)));
   CU(launch_roots_j0(c->jtab, count, roots, perturb, c->scratch, S(stream)));
   unsigned long long bits[2] = {0, 0};
@@ -846,6 +848,10 @@ int fhtb_coef_stats(const double* C, int64_t ldc, int32_t n_vec, int64_t n, int6
   if (n_vec == 0) return FHTB_OK;
   DevCtx* c;
   if (int r = get_ctx(&c)) return r;
+  // one caller at a time per process: the device buffer is shared (concurrent host threads,
+  // e.g. simulated ranks, would otherwise overwrite each other's rows before the copy-out)
+  static std::mutex stats_mu;
+  std::lock_guard<std::mutex> call_lk(stats_mu);
   {
     std::lock_guard<std::mutex> lk(g_mu);
     if (c->stats_cap < (size_t)n_vec) {
@@ -876,6 +882,7 @@ int fhtb_max_abs_diff(const double* a, double alpha, const double* b, int64_t n,
   if (n < 0 || !out_host) return fail(FHTB_EINVAL, "bad max_abs_diff arguments");
   DevCtx* c;
   if (int r = get_ctx(&c)) return r;
+  std::lock_guard<std::mutex> scratch_lk(g_scratch_mu);      // c->scratch is shared
   CU(cudaMemsetAsync(c->scratch, 0, 8, S(stream)));
   CU(launch_max_abs_diff(a, alpha, b, n, c->scratch, S(stream)));
   unsigned long long bits = 0;
