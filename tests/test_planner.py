@@ -180,3 +180,20 @@ def test_public_surface_matches_reference():
     assert expected <= names
     for n in expected - {"__version__"}:
         assert hasattr(fh, n)
+
+
+def test_order_windows_cover_universe_once():
+    """Engine universes wider than one device grid (16 orders inside 16
+    consecutive orders) are split greedily; every order lands in exactly one
+    window and each window satisfies both limits."""
+    from paper_1501_01652_b200.schlomilch import _MAX_UNIVERSE, _order_windows
+    for orders in ([0], list(range(11)), list(range(16)), list(range(17)), [0, 15], [0, 16], [3, 70, 5, 4, 64, 100],
+                   list(range(0, 40, 2)) + [70], list(range(55, 66)), [1023, 0]):
+        wins = _order_windows(orders)
+        flat = [o for w in wins for o in w]
+        assert sorted(flat) == sorted(set(orders))
+        assert len(flat) == len(set(flat))
+        for w in wins:
+            assert 1 <= len(w) <= _MAX_UNIVERSE and w[-1] - w[0] < _MAX_UNIVERSE and w == sorted(w)
+    assert _order_windows(list(range(16))) == [list(range(16))]
+    assert len(_order_windows(list(range(17)))) == 2
