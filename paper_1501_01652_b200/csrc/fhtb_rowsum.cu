@@ -358,7 +358,11 @@ cudaError_t launch_far_rowsum(const FarArgs& a, int logN2, int form, int n_units
     case 8: return rowsum_t<256, 8, 2>(a, n_units, st);
     case 9: return rowsum_t<512, 4, 2>(a, n_units, st);
     case 10: return rowsum_t<1024, 2, 2>(a, n_units, st);
-    case 11: return rowsum_t<2048, 1, 2>(a, n_units, st);
+    case 11:
+      // as at 4096 points: 8 points per thread (256 threads, 2 CTAs = 16 warps per SM, no
+      // spills) instead of 16 (128 threads at 255 registers, 8 warps)
+      if (g_far_variant & 0x20000) return rowsum_t<2048, 1, 2>(a, n_units, st);
+      return rowsum_t<2048, 1, 2, 8>(a, n_units, st);
     case 12:
       // 8 points per thread: 512 threads (16 warps) on the one CTA an SM holds,
       // one more shared-memory exchange (variant bit 17 selects 16 points, 8 warps)
